@@ -1,0 +1,272 @@
+"""Pins for the CPU oracle (``-m "not gpu"``).
+
+The oracle (oracle/polsar_oracle.c) is the plain definition of Z^-1, det Z and
+det Z^-1 (Eq. 3-5) and of the window sum (BASELINE configs[4]).  Each
+test below checks it against something other than itself: hand-derived worked
+examples, exact rational arithmetic, a brute-force Gauss-Jordan, LAPACK, closed
+forms and invariants.  A dropped term, a wrong sign / index / conjugation or a
+transposed operand in the oracle fails at least the exact-rational test and
+the Z*Z^-1 = I residual test.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from tests._exact import exact_inverse_det, packed_upper
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "worked_examples.txt")
+
+
+def rand_hpd(n, seed, ridge=0.1, scale_spread=False):
+    """Test-local random HPD matrices G G^H / 3 + ridge I (packed, float64)."""
+    rng = np.random.default_rng(seed)
+    g = (rng.standard_normal((n, 3, 3)) + 1j * rng.standard_normal((n, 3, 3))) / math.sqrt(2)
+    m = g @ np.conj(np.transpose(g, (0, 2, 1))) / 3 + ridge * np.eye(3)
+    if scale_spread:
+        m *= np.exp(rng.uniform(-10, 10, n))[:, None, None]
+    return pack(m)
+
+
+def pack(m):
+    return np.stack([m[:, 0, 0].real, m[:, 0, 1].real, m[:, 0, 1].imag,
+                     m[:, 0, 2].real, m[:, 0, 2].imag, m[:, 1, 1].real,
+                     m[:, 1, 2].real, m[:, 1, 2].imag, m[:, 2, 2].real]).astype(np.float64)
+
+
+def rand_kappa(n, seed, kappa):
+    """U diag(1, k^u, k) U^H with U Haar (numpy QR, phase-fixed): kappa_2 = k."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, 3, 3)) + 1j * rng.standard_normal((n, 3, 3))
+    q, r = np.linalg.qr(x)
+    ph = np.diagonal(r, axis1=1, axis2=2)
+    q = q * (ph / np.abs(ph))[:, None, :]
+    u = rng.uniform(0, 1, n)
+    lam = np.stack([np.ones(n), kappa ** u, np.full(n, float(kappa))], axis=1)
+    m = (q * lam[:, None, :]) @ np.conj(np.transpose(q, (0, 2, 1)))
+    return pack(m)
+
+
+def normwise(got9, ref9):
+    return np.max(np.abs(got9 - ref9), axis=0) / np.max(np.abs(ref9), axis=0)
+
+
+def parse_golden():
+    rows = []
+    for line in open(GOLDEN):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        name, zin, inv, det, idet = [s.strip() for s in line.split("|")]
+        rows.append((name, np.array(zin.split(), float), np.array(inv.split(), float),
+                     float(det), float(idet)))
+    return rows
+
+
+def test_extended_precision():
+    # the oracle must really evaluate in binary128 (inverse/det) and 80-bit
+    # long double (window) on this host
+    assert oracle.quad_mant_dig() == 113
+    assert oracle.ldbl_mant_dig() == 64
+
+
+@pytest.mark.parametrize("row", parse_golden(), ids=lambda r: r[0])
+def test_worked_examples(row):
+    name, zin, inv, det, idet = row
+    out = oracle.inv_det(zin.reshape(9, 1))
+    np.testing.assert_allclose(out[:9, 0], inv, rtol=0, atol=2e-16 * np.abs(inv).max())
+    assert out[9, 0] == pytest.approx(det, rel=1e-16, abs=0)
+    assert out[10, 0] == pytest.approx(idet, rel=2e-16, abs=0)
+    if name in ("identity", "diag245", "golden"):
+        # dyadic inputs with dyadic results: exact
+        assert np.array_equal(out[:9, 0], inv)
+        assert out[9, 0] == det and out[10, 0] == idet
+
+
+def test_exact_rational_random():
+    z = np.concatenate([rand_hpd(40, 1), rand_kappa(20, 2, 1e3)], axis=1)
+    out = oracle.inv_det(z)
+    for p in range(z.shape[1]):
+        inv, det = exact_inverse_det(z[:, p])
+        assert det.im == 0  # Hermitian => real determinant, exactly
+        ref = np.array(packed_upper(inv))
+        err = np.max(np.abs(out[:9, p] - ref)) / np.max(np.abs(ref))
+        assert err <= 1e-15, (p, err)
+        detf = float(det.re)
+        # one final rounding (2^-53) plus binary128 rounding of the
+        # expansion's terms, whose magnitude is bounded by 6 max|z|^3
+        terms = 6 * np.max(np.abs(z[:, p])) ** 3
+        bound = 1.2e-16 * abs(detf) + 32 * 2.0 ** -113 * terms
+        assert abs(out[9, p] - detf) <= bound
+        assert abs(out[10, p] - 1.0 / detf) <= 1.2e-16 / abs(detf) + bound / detf ** 2
+
+
+def test_exact_rational_lower_triangle_hermitian():
+    # the full exact inverse is Hermitian: the packed upper triangle determines it
+    z = rand_hpd(10, 3)
+    for p in range(z.shape[1]):
+        inv, _ = exact_inverse_det(z[:, p])
+        for r in range(3):
+            for c in range(3):
+                assert inv[r][c].re == inv[c][r].re and inv[r][c].im == -inv[c][r].im
+
+
+def test_det_imag_vanishes():
+    z = rand_hpd(5000, 4, scale_spread=True)
+    out, im = oracle.inv_det(z, with_imag=True)
+    scale = np.abs(z[0] * z[5] * z[8]) + np.abs(z).max(axis=0) ** 3
+    assert np.all(np.abs(im) <= 64 * 2.0 ** -64 * scale)
+
+
+def test_gauss_jordan_brute_force():
+    z = np.concatenate([rand_hpd(3000, 5), rand_kappa(3000, 6, 1e6)], axis=1)
+    out = oracle.inv_det(z)
+    inv, det = oracle.gauss_jordan(z)
+    k = oracle.kappa2(z)
+    # the brute force's full inverse is Hermitian up to rounding
+    herm = np.abs(inv - np.conj(np.transpose(inv, (0, 2, 1)))).max(axis=(1, 2))
+    assert np.all(herm <= 1e-15 * k * np.abs(inv).max(axis=(1, 2)))
+    gj9 = pack(inv)
+    err = normwise(out[:9], gj9)
+    assert np.all(err <= 1e-17 * k + 4e-16), err.max()
+    assert np.all(np.abs(det.imag) <= 1e-15 * np.abs(det.real) * k)
+    assert np.all(np.abs(out[9] - det.real) <= (1e-17 * k + 4e-16) * np.abs(det.real))
+
+
+def test_lapack_special_case():
+    z = rand_kappa(2000, 7, 1e4)
+    out = oracle.inv_det(z)
+    full = oracle.to_full(z)
+    inv = np.linalg.inv(full)
+    det = np.linalg.det(full)
+    assert np.all(normwise(out[:9], pack(inv)) <= 1e-12)
+    assert np.all(np.abs(out[9] - det.real) <= 1e-12 * np.abs(det.real))
+
+
+def test_residual_identity():
+    z = np.concatenate([rand_hpd(2000, 8), rand_kappa(2000, 9, 1e4)], axis=1)
+    out = oracle.inv_det(z)
+    k = oracle.kappa2(z)
+    res = oracle.residual(z, out[:9])
+    scale = np.abs(z).max(axis=0) * np.abs(out[:9]).max(axis=0)
+    assert np.all(res <= 8 * 2.2e-16 * scale + 1e-18 * k * scale)
+
+
+@pytest.mark.parametrize("m", [1, -3, 7])
+def test_power_of_two_scaling_exact(m):
+    z = rand_hpd(3000, 10, scale_spread=True)
+    k = 2.0 ** m
+    a = oracle.inv_det(z)
+    b = oracle.inv_det(z * k)
+    assert np.array_equal(b[:9], a[:9] / k)
+    assert np.array_equal(b[9], a[9] * k ** 3)
+    assert np.array_equal(b[10], a[10] / k ** 3)
+
+
+def test_det_times_inverse_det():
+    z = rand_hpd(5000, 11, scale_spread=True)
+    out = oracle.inv_det(z)
+    assert np.all(np.abs(out[9] * out[10] - 1.0) <= 4.5e-16)
+    assert np.all(out[9] > 0)
+
+
+def test_block_diagonal_closed_form():
+    rng = np.random.default_rng(12)
+    n = 1000
+    a = rng.uniform(1, 3, n)
+    d = rng.uniform(1, 3, n)
+    f = rng.uniform(0.1, 2, n)
+    b = rng.uniform(-0.7, 0.7, n) + 1j * rng.uniform(-0.7, 0.7, n)
+    z = np.stack([a, b.real, b.imag, 0 * a, 0 * a, d, 0 * a, 0 * a, f])
+    out = oracle.inv_det(z)
+    g = a * d - np.abs(b) ** 2
+    ref = np.stack([d / g, -b.real / g, -b.imag / g, 0 * a, 0 * a, a / g, 0 * a, 0 * a, 1 / f])
+    assert np.all(normwise(out[:9], ref) <= 1e-15)
+    np.testing.assert_allclose(out[9], g * f, rtol=1e-15)
+
+
+def test_rank_one_is_singular():
+    rng = np.random.default_rng(13)
+    s = rng.standard_normal((500, 3)) + 1j * rng.standard_normal((500, 3))
+    m = s[:, :, None] * np.conj(s[:, None, :])
+    z = pack(m)
+    out = oracle.inv_det(z)
+    adf = z[0] * z[5] * z[8]
+    assert np.all(np.abs(out[9]) <= 1e-15 * adf)
+
+
+# ---------------------------------------------------------------- window oracle
+
+def clipped_count(y, x, h, w, r):
+    return (min(h - 1, y + r) - max(0, y - r) + 1) * (min(w - 1, x + r) - max(0, x - r) + 1)
+
+
+def test_window_constant_image_exact():
+    h, w, r = 9, 11, 3
+    z0 = rand_hpd(1, 14)[:, 0]
+    z = np.repeat(z0[:, None], h * w, axis=1)
+    got = oracle.window(z, h, w, r, 4.0, 1.0)
+    ref = np.array([clipped_count(p // w, p % w, h, w, r) for p in range(h * w)], float)
+    assert np.array_equal(got, ref)
+
+
+def test_window_two_class_closed_form():
+    h, w, r, looks = 8, 10, 2, 4.0
+    za, zb = rand_hpd(2, 15)[:, 0], rand_hpd(2, 15)[:, 1]
+    xs = np.arange(h * w) % w
+    z = np.where(xs[None, :] < 5, za[:, None], zb[:, None])
+    got = oracle.window(z, h, w, r, looks, 1.0)
+    # d_AB from LAPACK log-determinants (independent of the oracle)
+    fa, fb = oracle.to_full(za[:, None])[0], oracle.to_full(zb[:, None])[0]
+    dab = looks * (np.linalg.slogdet((fa + fb) / 2)[1]
+                   - 0.5 * (np.linalg.slogdet(fa)[1] + np.linalg.slogdet(fb)[1]))
+    for p in range(h * w):
+        y, x = divmod(p, w)
+        ys = range(max(0, y - r), min(h, y + r + 1))
+        xr = range(max(0, x - r), min(w, x + r + 1))
+        same = sum(1 for _ in ys for xx in xr if (xx < 5) == (x < 5))
+        other = len(ys) * len(xr) - same
+        assert got[p] == pytest.approx(same + other * math.exp(-dab), rel=1e-13)
+
+
+def test_pair_distance_properties():
+    z = rand_kappa(200, 16, 1e3)
+    for p in range(0, 200, 2):
+        zi, zj = z[:, p], z[:, p + 1]
+        assert oracle.pair_distance(zi, zi, 4.0) == 0.0
+        dij = oracle.pair_distance(zi, zj, 4.0)
+        assert dij == pytest.approx(oracle.pair_distance(zj, zi, 4.0), rel=1e-15, abs=1e-18)
+        assert dij >= 0.0  # log-det concavity
+        # det is homogeneous: d_ij(k Z_i, k Z_j) = d_ij
+        assert oracle.pair_distance(3.7 * zi, 3.7 * zj, 4.0) == pytest.approx(dij, rel=1e-12, abs=1e-15)
+
+
+def test_window_brute_force_tiny():
+    h, w, r, looks, hh = 5, 6, 2, 4.0, 1.0
+    z = rand_kappa(h * w, 17, 50.0)
+    got = oracle.window(z, h, w, r, looks, hh)
+    full = oracle.to_full(z)
+    ld = np.log(np.linalg.det(full).real)
+    for p in range(h * w):
+        y, x = divmod(p, w)
+        acc = 0.0
+        for yy in range(max(0, y - r), min(h, y + r + 1)):
+            for xx in range(max(0, x - r), min(w, x + r + 1)):
+                q = yy * w + xx
+                ds = np.log(np.linalg.det((full[p] + full[q]) / 2).real)
+                acc += math.exp(-looks * (ds - 0.5 * (ld[p] + ld[q])) / hh)
+        assert got[p] == pytest.approx(acc, rel=1e-12)
+
+
+def test_window_power_form_equivalence():
+    # h = 1, L = 4: exp(-d_ij) = ((D_i/D_S)(D_j/D_S))^2 with D_S = det((Z_i+Z_j)/2)
+    # (the form the CUDA kernel may use) -- checked on the oracle's own d_ij.
+    z = rand_kappa(40, 18, 100.0)
+    full = oracle.to_full(z)
+    for p in range(0, 40, 2):
+        dij = oracle.pair_distance(z[:, p], z[:, p + 1], 4.0)
+        di, dj = np.linalg.det(full[p]).real, np.linalg.det(full[p + 1]).real
+        ds = np.linalg.det((full[p] + full[p + 1]) / 2).real
+        assert math.exp(-dij) == pytest.approx(((di / ds) * (dj / ds)) ** 2, rel=1e-12)
