@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: batched 3x3 Hermitian inverse + determinant
+(arXiv 1807.08084, Alg. 2) on B200.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c3] [--algo adjugate]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+  python bench.py --impl reference ...      # the CPU oracle, as it stands
+
+A step is one pass of the hot path over one batch: the K1 kernel
+(polsar_inv_det, Alg. 2) over this rank's pixels -- inverse (9 planes),
+det Z, det Z^-1 and the status plane -- with the inputs resident in HBM.
+Default workload: BASELINE configs[2] (c3), 10000 x 40000 fp32 L=4 Wishart
+pixels per GPU (weak scaling: rank r owns rows [r*10000, (r+1)*10000) of an
+N*10000-row image; --scaling strong splits one 10000-row image instead).
+Inputs (14.4 GB) and outputs (17.6 GB) are far larger than the 126 MB L2,
+so no flush is needed between steps; smaller configs flush L2 between steps.
+
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "matrices/s (inverse+det)"
+UNIT = "matrices/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="c3")
+    p.add_argument("--algo", choices=["adjugate", "cholesky"], default="adjugate")
+    p.add_argument("--plain", action="store_true", help="Alg. as printed in storage precision")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extras", action="store_true", help="skip the K2 / K3 side measurements")
+    p.add_argument("--no-status", action="store_true")
+    p.add_argument("--verify", action="store_true", help="sampled oracle check after timing")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def read_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def read_traffic(key):
+    """dram bytes per launch from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clock and throttle
+    reasons during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, device_index, period=0.01):
+        self.period = period
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz,
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b],
+                "samples": len(s)}
+
+
+def setup_dist(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    return world, rank, local
+
+
+def rows_for(rank, world, cfg, scaling):
+    if scaling == "weak":
+        H = cfg.height * world
+        return H, rank * cfg.height, (rank + 1) * cfg.height
+    H = cfg.height
+    return H, (rank * H) // world, ((rank + 1) * H) // world
+
+
+def bytes_per_matrix(esz, status):
+    return 20 * esz + (1 if status else 0)
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The CPU oracle (oracle/, as it stands) on the host cores, on a bounded
+    sample of the same workload per step; rank 0 only."""
+    world, rank, _ = setup_dist(args)
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    from paper_1807_08084_b200 import configs, wishart
+
+    cfg = configs.get(args.config)
+    cores = len(os.sched_getaffinity(0))
+    sample = min(cfg.n, 1 << 22)  # 4.2M matrices per step (~0.3-0.6 s on 16 cores)
+    rows = max(1, sample // cfg.width)
+    tab = cfg.table()
+    z = wishart.generate_cpu(cfg, 0, rows, table=tab)[:, :sample].copy()
+    for _ in range(args.warmup):
+        oracle.inv_det_threaded(z, cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.inv_det_threaded(z, cores)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = sample / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "binary128 (oracle)", "data": "synthetic (seeded Wishart, host twin generator)",
+        "config": {"workload": f"{cfg.name} (BASELINE configs[{cfg.baseline_index}]) bounded sample",
+                   "sample_pixels": sample, "looks": cfg.looks, "storage": cfg.dtype},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"first {sample} pixels of {cfg.name}, per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1807_08084_b200 as P
+    from paper_1807_08084_b200 import configs, wishart
+
+    world, rank, local = setup_dist(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = configs.get(args.config)
+    if cfg.radius:
+        raise SystemExit("window configs are measured as an extra; pick c1..c4 for --config")
+    H, r0, r1 = rows_for(rank, world, cfg, args.scaling)
+    n = (r1 - r0) * cfg.width
+    tdt = torch.float32 if cfg.dtype == "float32" else torch.float64
+    esz = 4 if tdt == torch.float32 else 8
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        tab = cfg.table(H)
+        z = wishart.generate(cfg, r0, r1, device=dev, table=tab, height=H)
+        out = torch.empty((11, n), dtype=tdt, device=dev)
+        status = None if args.no_status else torch.empty(n, dtype=torch.uint8, device=dev)
+    stream.synchronize()
+    fn = P.polsar_inv_det if args.algo == "adjugate" else P.polsar_inv_det_cholesky
+
+    l2_flush = None
+    if n * bytes_per_matrix(esz, status is not None) < 4 * 126 * 2 ** 20:
+        l2_flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        fn(z, out, status, plain=args.plain, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    stream.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev.index if dev.index is not None else 0)
+    with sampler:
+        for i in range(args.steps):
+            if l2_flush is not None:
+                with torch.cuda.stream(stream):
+                    l2_flush.fill_(i & 0xFF)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        stream.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per_step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_local = sum(per_step_ms) / 1e3  # kernel-only time of the K timed steps
+    t_max = t_local
+    if world > 1:
+        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    total = n * world
+    value = total * args.steps / t_max
+    ms_per_step = t_max / args.steps * 1e3
+
+    # roofline of the (only) kernel of the step
+    bpm = bytes_per_matrix(esz, status is not None)
+    achieved = n * bpm / (t_local / args.steps) / 1e9
+    peak, peak_src = read_peaks()
+    key = f"{cfg.name}:{args.algo}:{'plain' if args.plain else 'default'}"
+    traffic = read_traffic(key)
+
+    # multi-GPU verification reduction (outside the timed region): checksum
+    # of all outputs + status counts, NCCL all_reduce (SUM wraps like uint64)
+    res = P.polsar_checksum(out, n, 11, r0 * cfg.width, status, stream=stream)
+    stream.synchronize()
+    if world > 1:
+        dist.all_reduce(res, op=dist.ReduceOp.SUM)
+    checksum = int(res[0].item()) & 0xFFFFFFFFFFFFFFFF
+    counts = [int(x) for x in res[1:].tolist()]
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f32" if (args.plain and tdt == torch.float32) else "f64",
+        "data": "synthetic (seeded Wishart, BASELINE law)",
+        "config": {
+            "workload": f"{cfg.name}: BASELINE configs[{cfg.baseline_index}] "
+                        f"{cfg.height}x{cfg.width} {cfg.dtype} L={cfg.looks} per GPU",
+            "algo": "Alg. 2 (adjugate)" if args.algo == "adjugate" else "Alg. 1 (Cholesky, l21 fixed)",
+            "storage": cfg.dtype, "mode": "plain" if args.plain else "default",
+            "pixels_per_gpu": n, "image_rows": H, "status_plane": status is not None,
+            "l2": "flushed between steps" if l2_flush is not None else
+                  f"inputs+outputs {n * bpm / 1e9:.1f} GB per step >> 126 MB L2 (no flush)",
+            "parallelism": f"dp{world} (pixel rows)",
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src, "bytes_per_matrix": bpm},
+        "clocks": sampler.summary(),
+        "gpu_launches": args.steps,
+        "checksum": f"{checksum:016x}", "status_counts": counts,
+        "t_step_ms": {"min": min(per_step_ms), "avg": sum(per_step_ms) / len(per_step_ms),
+                      "max": max(per_step_ms)},
+    }
+
+    # ---------------- e2e: the public host-buffer entry point, copies inside
+    if not args.no_e2e:
+        line["e2e"] = measure_e2e(args, P, torch, dist, world, z, n, tdt, esz, dev, cfg)
+    # ---------------- side measurements (same run): K2 and K3
+    if not args.no_extras and rank == 0 and world == 1:
+        line["extras"] = measure_extras(args, P, torch, z, out, status, stream, dev, esz)
+    # ---------------- cpu baseline: the oracle on this host (rank 0, N=1)
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = measure_cpu_baseline(z, cfg)
+    if args.verify:
+        line["verify"] = verify_sample(P, z, out, status, cfg, r0)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_e2e(args, P, torch, dist, world, z, n, tdt, esz, dev, cfg):
+    zh = torch.empty((9, n), dtype=tdt).pin_memory()
+    zh.copy_(z)
+    oh = torch.empty((11, n), dtype=tdt).pin_memory()
+    sh = torch.empty(n, dtype=torch.uint8).pin_memory()
+    ws = torch.empty(3 << 30, dtype=torch.uint8, device=dev)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
+    algo = 0 if args.algo == "adjugate" else 1
+    P.polsar_inv_det_host(zh, oh, sh, ws, streams, algo=algo, plain=args.plain)  # warm-up
+    times = []
+    for _ in range(args.e2e_steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(streams[0])
+        P.polsar_inv_det_host(zh, oh, sh, ws, streams, algo=algo, plain=args.plain)
+        t1.record(streams[2])
+        t1.synchronize()
+        times.append(t0.elapsed_time(t1) / 1e3)
+    t = sum(times) / len(times)
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    del ws
+    return {"value": n * world / t, "unit": UNIT, "h2d_bytes_per_step": 9 * n * esz,
+            "d2h_bytes_per_step": 11 * n * esz + n, "steps": args.e2e_steps,
+            "ms_per_step": t * 1e3,
+            "path": "polsar_inv_det_host: pinned host -> 3-slot chunked H2D/kernel/D2H pipeline"}
+
+
+def _time_kernel(torch, stream, fn, steps, warm=3):
+    for _ in range(warm):
+        fn()
+    stream.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        fn()
+    b.record(stream)
+    b.synchronize()
+    return a.elapsed_time(b) / 1e3 / steps
+
+
+def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
+    from paper_1807_08084_b200 import configs, wishart
+    n = z.shape[1]
+    peak, _ = read_peaks()
+    bpm = bytes_per_matrix(esz, status is not None)
+    res = {}
+    steps = max(5, min(args.steps, 20))
+    for algo, fn in (("adjugate", P.polsar_inv_det), ("cholesky", P.polsar_inv_det_cholesky)):
+        for plain in (False, True):
+            t = _time_kernel(torch, stream, lambda: fn(z, out, status, plain=plain, stream=stream), steps)
+            gbs = n * bpm / t / 1e9
+            res[f"{algo}{'_plain' if plain else ''}"] = {
+                "matrices_per_s": n / t, "ms": t * 1e3, "GB/s": gbs, "frac_hbm": gbs / peak}
+    # K3: BASELINE configs[4] window sum on one GPU
+    c5 = configs.get("c5")
+    with torch.cuda.stream(stream):
+        z5 = wishart.generate(c5, device=dev)
+        code = P.dtype_code(z5.dtype)
+        ws = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, code),
+                         dtype=torch.uint8, device=dev)
+        w5 = torch.empty(c5.n, dtype=z5.dtype, device=dev)
+    stream.synchronize()
+    pairs = window_pairs(c5.height, c5.width, c5.radius)
+    for plain in (False, True):
+        t = _time_kernel(torch, stream, lambda: P.polsar_window_distance(
+            z5, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, w5,
+            plain=plain, stream=stream), steps)
+        res[f"window_c5{'_plain' if plain else ''}"] = {
+            "pairs_per_s": pairs / t, "ms": t * 1e3, "pairs": pairs,
+            "mode": "fp32 storage, fp32 weight, " + ("fp32 pair det" if plain else "fp64 pair det")}
+    return res
+
+
+def window_pairs(h, w, r):
+    def clipped(n):
+        import numpy as np
+        i = np.arange(n)
+        return int(np.sum(np.minimum(n - 1, i + r) - np.maximum(0, i - r) + 1))
+    return clipped(h) * clipped(w)
+
+
+def measure_cpu_baseline(z, cfg):
+    """The oracle (oracle/, binary128 cofactor expansion, as it stands) on
+    this box's host cores, on a bounded sample of the same workload."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    probe = z[:, :1 << 18].cpu().numpy()
+    t0 = time.perf_counter()
+    oracle.inv_det_threaded(probe, cores)
+    rate = probe.shape[1] / (time.perf_counter() - t0)
+    sample = int(min(z.shape[1], max(1 << 20, rate * 10.0)))  # ~10 s wall on all cores
+    zs = z[:, :sample].cpu().numpy()
+    t0 = time.perf_counter()
+    oracle.inv_det_threaded(zs, cores)
+    t = time.perf_counter() - t0
+    return {"value": sample / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {sample} pixels of this rank's {cfg.name} input (D2H copy), "
+                      f"{t:.1f} s wall on {cores} threads"}
+
+
+def verify_sample(P, z, out, status, cfg, r0):
+    import numpy as np
+
+    import oracle
+    rng = np.random.default_rng(1)
+    n = z.shape[1]
+    idx = np.unique(rng.integers(0, n, 20000))
+    ii = __import__("torch").as_tensor(idx, device=z.device)
+    zs = z[:, ii].cpu().numpy()
+    ref = oracle.inv_det(zs)
+    got = out[:, ii].cpu().numpy().astype(np.float64)
+    k = oracle.kappa2(zs)
+    m = k <= 1e4
+    inv = np.max(np.abs(got[:9] - ref[:9]), axis=0) / np.max(np.abs(ref[:9]), axis=0)
+    det = np.abs(got[9] - ref[9]) / np.abs(ref[9])
+    return {"pixels": int(idx.size), "kappa_le_1e4": int(m.sum()),
+            "max_rel_inv": float(inv[m].max()), "max_rel_det": float(det[m].max())}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

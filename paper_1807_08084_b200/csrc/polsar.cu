@@ -1,0 +1,832 @@
+// polsar.cu -- B200 (sm_100a) kernels and C-ABI for arXiv 1807.08084:
+// batched inverse + determinant of 3x3 Hermitian PD PolSAR matrices.
+//
+//   K1  polsar_inv_det           Alg. 2, HBM-streaming
+//   K2  polsar_inv_det_cholesky  Alg. 1, l21 corrected
+//   K3  polsar_window_distance   23x23 search-window log-det distance sum
+//   R1  polsar_checksum          order-independent output hash + status counts
+//   E2E polsar_inv_det_host      chunked H2D / kernel / D2H pipeline
+//
+// Layout, ownership and error conventions: include/polsar.h.  Design and
+// roofline notes: DESIGN.md.  Nothing here is shared with oracle/.
+//
+// Bit-stability: every floating-point operation of the per-matrix device
+// functions is an explicit round-to-nearest intrinsic (__fma_rn, __dmul_rn,
+// __dadd_rn, ...), so ptxas cannot contract or reassociate differently in the
+// vector body and the scalar tail: both yield identical bits.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <type_traits>
+
+#include "../../include/polsar.h"
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+thread_local const char* g_last_error = "";
+
+int fail(int code, const char* msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int launch_check(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_last_error = what;
+        return POLSAR_ECUDA;
+    }
+    g_last_error = "";
+    return POLSAR_OK;
+}
+
+// ----------------------------------------------------- rounding intrinsics
+// Overloads so one template body serves fp32 and fp64 arithmetic.
+__device__ __forceinline__ double MUL(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float MUL(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double ADD(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float ADD(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double SUB(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float SUB(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double FMA(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float FMA(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double RCP(double a) { return __drcp_rn(a); }
+__device__ __forceinline__ float RCP(float a) { return __frcp_rn(a); }
+__device__ __forceinline__ double SQRT(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ float SQRT(float a) { return __fsqrt_rn(a); }
+
+// ------------------------------------------------------ streaming HBM I/O
+// Loads: read-only path, no L1 allocation (each byte is touched once).
+// Stores: .cs (evict-first streaming).  16-byte forms for the vector path.
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream(float4* p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ void st_stream(double2* p, double2 v) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_stream(float* p, float v) {
+    asm volatile("st.global.cs.f32 [%0], %1;" :: "l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_stream(double* p, double v) {
+    asm volatile("st.global.cs.f64 [%0], %1;" :: "l"(p), "d"(v) : "memory");
+}
+
+// ------------------------------------------------------------ matrix types
+template <typename T>
+struct H9 {  // packed Hermitian
+    T a, br, bi, cr, ci, d, er, ei, f;
+};
+
+template <typename T>
+struct R11 {  // 9 inverse components, det, det^-1, status
+    T v[11];
+    uint8_t status;
+};
+
+// tau * a*d*f, tau = 16 u_in (R-5)
+template <typename S>
+struct Tau;
+template <>
+struct Tau<float> {
+    static constexpr double v = 16.0 * 5.9604644775390625e-08;  // 16 * 2^-24
+};
+template <>
+struct Tau<double> {
+    static constexpr double v = 16.0 * 1.1102230246251565e-16;  // 16 * 2^-53
+};
+
+template <typename T>
+__device__ __forceinline__ bool finite_pos(T x) {
+    return x > T(0) && x < T(INFINITY);
+}
+
+// ====================================================== Alg. 2 (proposed)
+// PAPER.md:480-545.  Step 1 cofactors (495-503, Eq. 3), step 2 determinant
+// from real parts only (505-517, Eq. 6), step 3 t = 1/det (519-520), step 4
+// scale the six entries by t (523-528).  Arithmetic type T, one rounding per
+// operation, FMA where the hardware fuses.
+template <typename T>
+__device__ __forceinline__ void alg2_plain(const H9<T>& m, T* o, T& det, T& t) {
+    // step 1: cofactors (stored in the output slots, as Alg. 2 does)
+    T ai = FMA(m.d, m.f, -FMA(m.er, m.er, MUL(m.ei, m.ei)));       // d f - |e|^2
+    T bir = FMA(m.cr, m.er, FMA(m.ci, m.ei, -MUL(m.br, m.f)));      // Re(c conj e - b f)
+    T bii = FMA(m.ci, m.er, -FMA(m.cr, m.ei, MUL(m.bi, m.f)));      // Im(c conj e - b f)
+    T cir = FMA(m.br, m.er, -FMA(m.bi, m.ei, MUL(m.cr, m.d)));      // Re(b e - c d)
+    T cii = FMA(m.br, m.ei, FMA(m.bi, m.er, -MUL(m.ci, m.d)));      // Im(b e - c d)
+    T di = FMA(m.a, m.f, -FMA(m.cr, m.cr, MUL(m.ci, m.ci)));        // a f - |c|^2
+    T eir = FMA(m.cr, m.br, FMA(m.ci, m.bi, -MUL(m.a, m.er)));      // Re(c conj b - a e)
+    T eii = FMA(m.ci, m.br, -FMA(m.cr, m.bi, MUL(m.a, m.ei)));      // Im(c conj b - a e)
+    T fi = FMA(m.a, m.d, -FMA(m.br, m.br, MUL(m.bi, m.bi)));        // a d - |b|^2
+    // step 2: det = a a_i + Re b Re b_i + Im b Im b_i + Re c Re c_i + Im c Im c_i
+    det = FMA(m.a, ai, FMA(m.br, bir, FMA(m.bi, bii, FMA(m.cr, cir, MUL(m.ci, cii)))));
+    // step 3
+    t = RCP(det);
+    // step 4
+    o[0] = MUL(t, ai);
+    o[1] = MUL(t, bir);
+    o[2] = MUL(t, bii);
+    o[3] = MUL(t, cir);
+    o[4] = MUL(t, cii);
+    o[5] = MUL(t, di);
+    o[6] = MUL(t, eir);
+    o[7] = MUL(t, eii);
+    o[8] = MUL(t, fi);
+}
+
+// ---- error-free transformations (fp64) for the accurate Alg. 2 (R-16)
+struct dd {
+    double hi, lo;
+};
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+    s = __dadd_rn(a, b);
+    double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// x1 y1 + x2 y2 + x3 y3 as an unevaluated sum hi + lo (Dot2 of Ogita, Rump &
+// Oishi 2005 with FMA two-products): |hi + lo - exact| <= ~3u^2 sum|x y|.
+__device__ __forceinline__ dd dot3(double x1, double y1, double x2, double y2, double x3,
+                                   double y3) {
+    double p1 = __dmul_rn(x1, y1), e1 = __fma_rn(x1, y1, -p1);
+    double p2 = __dmul_rn(x2, y2), e2 = __fma_rn(x2, y2, -p2);
+    double p3 = __dmul_rn(x3, y3), e3 = __fma_rn(x3, y3, -p3);
+    double s, t1, s2, t2;
+    two_sum(p1, p2, s, t1);
+    two_sum(s, p3, s2, t2);
+    double lo = __dadd_rn(__dadd_rn(e1, e2), __dadd_rn(e3, __dadd_rn(t1, t2)));
+    dd r;
+    two_sum(s2, lo, r.hi, r.lo);
+    return r;
+}
+
+// Alg. 2 with every cofactor carried as hi + lo and the step-2 determinant
+// summed with Dot2 over (x_k, hi_k) plus the x_k lo_k terms: det and every
+// inverse entry come out within a few ulp, independent of the cancellation
+// (the plain form loses ~kappa^2 u for matrices with one dominant eigenvalue).
+__device__ __forceinline__ void alg2_accurate(const H9<double>& m, double* o, double& det,
+                                              double& t) {
+    // step 1 (Eq. 3), each cofactor as a 3-term dot product
+    dd ai = dot3(m.d, m.f, -m.er, m.er, -m.ei, m.ei);
+    dd bir = dot3(m.cr, m.er, m.ci, m.ei, -m.br, m.f);
+    dd bii = dot3(m.ci, m.er, -m.cr, m.ei, -m.bi, m.f);
+    dd cir = dot3(m.br, m.er, -m.bi, m.ei, -m.cr, m.d);
+    dd cii = dot3(m.br, m.ei, m.bi, m.er, -m.ci, m.d);
+    dd di = dot3(m.a, m.f, -m.cr, m.cr, -m.ci, m.ci);
+    dd eir = dot3(m.cr, m.br, m.ci, m.bi, -m.a, m.er);
+    dd eii = dot3(m.ci, m.br, -m.cr, m.bi, -m.a, m.ei);
+    dd fi = dot3(m.a, m.d, -m.br, m.br, -m.bi, m.bi);
+    // step 2 (Eq. 6): det = sum_k x_k (hi_k + lo_k), compensated
+    double p0 = __dmul_rn(m.a, ai.hi), q0 = __fma_rn(m.a, ai.hi, -p0);
+    double p1 = __dmul_rn(m.br, bir.hi), q1 = __fma_rn(m.br, bir.hi, -p1);
+    double p2 = __dmul_rn(m.bi, bii.hi), q2 = __fma_rn(m.bi, bii.hi, -p2);
+    double p3 = __dmul_rn(m.cr, cir.hi), q3 = __fma_rn(m.cr, cir.hi, -p3);
+    double p4 = __dmul_rn(m.ci, cii.hi), q4 = __fma_rn(m.ci, cii.hi, -p4);
+    double s, r1, r2, r3, r4;
+    two_sum(p0, p1, s, r1);
+    two_sum(s, p2, s, r2);
+    two_sum(s, p3, s, r3);
+    two_sum(s, p4, s, r4);
+    double err = __dadd_rn(__dadd_rn(__dadd_rn(q0, q1), __dadd_rn(q2, q3)),
+                           __dadd_rn(q4, __dadd_rn(__dadd_rn(r1, r2), __dadd_rn(r3, r4))));
+    err = __fma_rn(m.a, ai.lo, err);
+    err = __fma_rn(m.br, bir.lo, err);
+    err = __fma_rn(m.bi, bii.lo, err);
+    err = __fma_rn(m.cr, cir.lo, err);
+    err = __fma_rn(m.ci, cii.lo, err);
+    det = __dadd_rn(s, err);
+    // step 3
+    t = __drcp_rn(det);
+    // step 4
+    o[0] = __dmul_rn(t, ai.hi);
+    o[1] = __dmul_rn(t, bir.hi);
+    o[2] = __dmul_rn(t, bii.hi);
+    o[3] = __dmul_rn(t, cir.hi);
+    o[4] = __dmul_rn(t, cii.hi);
+    o[5] = __dmul_rn(t, di.hi);
+    o[6] = __dmul_rn(t, eir.hi);
+    o[7] = __dmul_rn(t, eii.hi);
+    o[8] = __dmul_rn(t, fi.hi);
+}
+
+// ===================================================== Alg. 1 (Cholesky)
+// PAPER.md:279-378 with l21 = (conj(e) - l20 conj(l10)) v1 (R-1).  Complex
+// quantities as (re, im) pairs; l_kk real positive (R-4).
+template <typename T>
+__device__ __forceinline__ bool alg1(const H9<T>& m, T* o, T& det, T& tdet) {
+    // step 1: L and v_k
+    T l00 = SQRT(m.a);
+    T v0 = RCP(l00);
+    T l10r = MUL(m.br, v0), l10i = MUL(-m.bi, v0);  // conj(b) v0
+    T l20r = MUL(m.cr, v0), l20i = MUL(-m.ci, v0);  // conj(c) v0
+    T r1 = FMA(-l10r, l10r, FMA(-l10i, l10i, m.d));  // d - |l10|^2
+    T l11 = SQRT(r1);
+    T v1 = RCP(l11);
+    // conj(e) - l20 conj(l10)
+    T ur = SUB(m.er, FMA(l20r, l10r, MUL(l20i, l10i)));
+    T ui = SUB(-m.ei, FMA(l20i, l10r, -MUL(l20r, l10i)));
+    T l21r = MUL(ur, v1), l21i = MUL(ui, v1);
+    T r2 = FMA(-l21r, l21r, FMA(-l21i, l21i, FMA(-l20r, l20r, FMA(-l20i, l20i, m.f))));
+    T l22 = SQRT(r2);
+    T v2 = RCP(l22);
+    // step 2: T = L^-1
+    T v01 = MUL(v0, v1);
+    T t10r = MUL(-l10r, v01), t10i = MUL(-l10i, v01);
+    T wr = FMA(l21r, l10r, -MUL(l21i, l10i));  // l21 l10
+    T wi = FMA(l21r, l10i, MUL(l21i, l10r));
+    T v02 = MUL(v2, v0);
+    T t20r = MUL(v02, FMA(wr, v1, -l20r));
+    T t20i = MUL(v02, FMA(wi, v1, -l20i));
+    T v12 = MUL(v1, v2);
+    T t21r = MUL(-l21r, v12), t21i = MUL(-l21i, v12);
+    // step 3: det = (l00 l11 l22)^2; det^-1 = (v0 v1 v2)^2 (R-14)
+    T pl = MUL(MUL(l00, l11), l22);
+    det = MUL(pl, pl);
+    T pv = MUL(v01, v2);
+    tdet = MUL(pv, pv);
+    // step 4: A^-1 = T^H T
+    o[0] = FMA(v0, v0, FMA(t10r, t10r, FMA(t10i, t10i, FMA(t20r, t20r, MUL(t20i, t20i)))));
+    o[1] = FMA(t10r, v1, FMA(t20r, t21r, MUL(t20i, t21i)));    // Re(conj t10 v1 + conj t20 t21)
+    o[2] = FMA(-t10i, v1, FMA(t20r, t21i, -MUL(t20i, t21r)));  // Im
+    o[3] = MUL(t20r, v2);                                      // conj(t20) v2
+    o[4] = MUL(-t20i, v2);
+    o[5] = FMA(v1, v1, FMA(t21r, t21r, MUL(t21i, t21i)));
+    o[6] = MUL(t21r, v2);  // conj(t21) v2
+    o[7] = MUL(-t21i, v2);
+    o[8] = MUL(v2, v2);
+    // radicands must be positive and finite (R-5)
+    return finite_pos(m.a) && finite_pos(r1) && finite_pos(r2);
+}
+
+// ------------------------------------------------------------------ modes
+// storage S, arithmetic per dtype code (include/polsar.h)
+enum { ALGO_ADJ = 0, ALGO_CHOL = 1 };
+enum { MATH_F64 = 0, MATH_F64_EFT = 1, MATH_F32 = 2 };
+
+template <typename S, int ALGO, int MATH>
+__device__ __forceinline__ void solve_one(const S* in, S* out, uint8_t& st) {
+    typedef typename std::conditional<MATH == MATH_F32, float, double>::type T;
+    H9<T> m;
+    m.a = (T)in[0];
+    m.br = (T)in[1];
+    m.bi = (T)in[2];
+    m.cr = (T)in[3];
+    m.ci = (T)in[4];
+    m.d = (T)in[5];
+    m.er = (T)in[6];
+    m.ei = (T)in[7];
+    m.f = (T)in[8];
+    T o[9], det, t;
+    bool pd = true;
+    if constexpr (ALGO == ALGO_ADJ) {
+        if constexpr (MATH == MATH_F64_EFT)
+            alg2_accurate(m, o, det, t);
+        else
+            alg2_plain<T>(m, o, det, t);
+    } else {
+        pd = alg1<T>(m, o, det, t);
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) out[k] = (S)o[k];
+    out[9] = (S)det;
+    out[10] = (S)t;
+    // full-rank check as a scaled threshold (R-5)
+    T thr = MUL(MUL(MUL((T)Tau<S>::v, m.a), m.d), m.f);
+    bool ok = (det > thr) && finite_pos(det) && finite_pos(t);
+    st = !pd ? (uint8_t)POLSAR_STATUS_NOT_PD : (ok ? (uint8_t)POLSAR_STATUS_OK
+                                                   : (uint8_t)POLSAR_STATUS_SINGULAR);
+}
+
+// --------------------------------------------------------------- K1 / K2
+// Vector body: each thread owns VEC consecutive pixels, reads one 16-byte
+// vector per input plane (9 x LDG.128) and writes one per output plane
+// (11 x STG.128), plus VEC status bytes.  Grid-stride over groups.
+template <typename S>
+struct Vec;
+template <>
+struct Vec<float> {
+    typedef float4 type;
+    static constexpr int n = 4;
+};
+template <>
+struct Vec<double> {
+    typedef double2 type;
+    static constexpr int n = 2;
+};
+
+template <typename V, typename S>
+__device__ __forceinline__ void unpack(const V& v, S* x);
+template <>
+__device__ __forceinline__ void unpack<float4, float>(const float4& v, float* x) {
+    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void unpack<double2, double>(const double2& v, double* x) {
+    x[0] = v.x; x[1] = v.y;
+}
+__device__ __forceinline__ float4 pack4(const float* x) { return make_float4(x[0], x[1], x[2], x[3]); }
+__device__ __forceinline__ double2 pack2(const double* x) { return make_double2(x[0], x[1]); }
+__device__ __forceinline__ float4 packv(const float* x, float4*) { return pack4(x); }
+__device__ __forceinline__ double2 packv(const double* x, double2*) { return pack2(x); }
+
+template <typename S, int ALGO, int MATH>
+__global__ void __launch_bounds__(256)
+k_inv_det_vec(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
+              int64_t n_groups, int64_t ld) {
+    typedef typename Vec<S>::type V;
+    constexpr int W = Vec<S>::n;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_groups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = g * W;
+        S in[9][W];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) unpack<V, S>(ld_stream(reinterpret_cast<const V*>(z + k * ld + p)), in[k]);
+        S res[11][W];
+        uint8_t st[W];
+#pragma unroll
+        for (int v = 0; v < W; ++v) {
+            S x[9], y[11];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) x[k] = in[k][v];
+            solve_one<S, ALGO, MATH>(x, y, st[v]);
+#pragma unroll
+            for (int k = 0; k < 11; ++k) res[k][v] = y[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 11; ++k)
+            st_stream(reinterpret_cast<V*>(out + k * ld + p), packv(res[k], (V*)nullptr));
+        if (status) {
+            if (W == 4) {
+                uint32_t w = (uint32_t)st[0] | ((uint32_t)st[1 % W] << 8) |
+                             ((uint32_t)st[2 % W] << 16) | ((uint32_t)st[3 % W] << 24);
+                asm volatile("st.global.cs.u32 [%0], %1;" :: "l"(status + p), "r"(w) : "memory");
+            } else {
+                uint16_t w = (uint16_t)(st[0] | (st[1 % W] << 8));
+                asm volatile("st.global.cs.u16 [%0], %1;" :: "l"(status + p), "h"(w) : "memory");
+            }
+        }
+    }
+}
+
+// Scalar path: misaligned planes and the ragged tail; same solve_one.
+template <typename S, int ALGO, int MATH>
+__global__ void __launch_bounds__(256)
+k_inv_det_scalar(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
+                 int64_t begin, int64_t end, int64_t ld) {
+    for (int64_t p = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < end;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        S x[9], y[11];
+        uint8_t st;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) x[k] = ld_stream(z + k * ld + p);
+        solve_one<S, ALGO, MATH>(x, y, st);
+#pragma unroll
+        for (int k = 0; k < 11; ++k) st_stream(out + k * ld + p, y[k]);
+        if (status) status[p] = st;
+    }
+}
+
+int g_num_sms = 0;
+
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+int grid_for(int64_t work, int threads) {
+    // enough CTAs for every SM to hold its resident maximum several times
+    // over; beyond that the grid-stride loop takes over
+    int64_t need = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)num_sms() * 64;
+    if (need > cap) need = cap;
+    return (int)(need < 1 ? 1 : need);
+}
+
+template <typename S, int ALGO, int MATH>
+int launch_inv_det(const void* zv, void* outv, uint8_t* status, int64_t n, int64_t ld,
+                   cudaStream_t s) {
+    const S* z = (const S*)zv;
+    S* out = (S*)outv;
+    constexpr int W = Vec<S>::n;
+    bool aligned = ((uintptr_t)z % 16 == 0) && ((uintptr_t)out % 16 == 0) && (ld % W == 0) &&
+                   (status == nullptr || (uintptr_t)status % W == 0);
+    int64_t n_vec = aligned ? (n / W) * W : 0;
+    if (n_vec > 0) {
+        int64_t groups = n_vec / W;
+        k_inv_det_vec<S, ALGO, MATH><<<grid_for(groups, 256), 256, 0, s>>>(z, out, status, groups, ld);
+    }
+    if (n > n_vec) {
+        k_inv_det_scalar<S, ALGO, MATH>
+            <<<grid_for(n - n_vec, 256), 256, 0, s>>>(z, out, status, n_vec, n, ld);
+    }
+    return launch_check(ALGO == ALGO_ADJ ? "polsar_inv_det: launch failed"
+                                         : "polsar_inv_det_cholesky: launch failed");
+}
+
+template <int ALGO>
+int dispatch_inv_det(const void* z, void* out, uint8_t* status, int64_t n, int64_t ld, int dtype,
+                     void* stream) {
+    if (n < 0) return fail(POLSAR_EINVAL, "n < 0");
+    if (ld < n) return fail(POLSAR_EINVAL, "ld < n");
+    if (n == 0) return POLSAR_OK;
+    if (!z || !out) return fail(POLSAR_EINVAL, "null z or out");
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (dtype) {
+        case POLSAR_F32: return launch_inv_det<float, ALGO, MATH_F64>(z, out, status, n, ld, s);
+        case POLSAR_F64:
+            return ALGO == ALGO_ADJ ? launch_inv_det<double, ALGO, MATH_F64_EFT>(z, out, status, n, ld, s)
+                                    : launch_inv_det<double, ALGO, MATH_F64>(z, out, status, n, ld, s);
+        case POLSAR_F32_PLAIN: return launch_inv_det<float, ALGO, MATH_F32>(z, out, status, n, ld, s);
+        case POLSAR_F64_PLAIN: return launch_inv_det<double, ALGO, MATH_F64>(z, out, status, n, ld, s);
+        default: return fail(POLSAR_EINVAL, "bad dtype");
+    }
+}
+
+// ==================================================== K3: window distance
+// K3a: per-pixel det Z_i (Eq. 6) into the workspace (fp64).
+// K3b: one CTA per TY x TX output tile; the (TY+2R) x (TX+2R) halo of Z and
+// D is staged in shared memory as fp64 planes; each thread owns RB
+// vertically adjacent output pixels and walks the window, reusing every
+// staged Z_j for all of its pixels within reach.  Per pair (R-12, BASELINE
+// configs[4]):  S = Z_i + Z_j  (exact in fp64 for fp32 storage),
+//   D_S = det(S)/8 = det((Z_i+Z_j)/2) by Eq. 6 (only a_c, b_c, c_c needed),
+//   r = (D_S / D_i)(D_S / D_j),  exp(-d_ij/h) = r^(-L/(2h)).
+constexpr int K3_TX = 32;
+constexpr int K3_TY = 16;
+constexpr int K3_RB = 2;                          // output rows per thread
+constexpr int K3_THREADS = K3_TX * K3_TY / K3_RB;  // 256
+
+template <typename T>
+__device__ __forceinline__ T det_eq6(T a, T br, T bi, T cr, T ci, T d, T er, T ei, T f) {
+    T ac = FMA(d, f, -FMA(er, er, MUL(ei, ei)));
+    T bcr = FMA(cr, er, FMA(ci, ei, -MUL(br, f)));
+    T bci = FMA(ci, er, -FMA(cr, ei, MUL(bi, f)));
+    T ccr = FMA(br, er, -FMA(bi, ei, MUL(cr, d)));
+    T cci = FMA(br, ei, FMA(bi, er, -MUL(ci, d)));
+    return FMA(a, ac, FMA(br, bcr, FMA(bi, bci, FMA(cr, ccr, MUL(ci, cci)))));
+}
+
+// K3a: g_i = 1 / (8 det Z_i) per slab pixel (det by Eq. 6 in T).
+template <typename S, typename T, typename WT>
+__global__ void __launch_bounds__(256)
+k_window_prep(const S* __restrict__ z, int64_t ld, int64_t n, WT* __restrict__ g) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        T v[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) v[k] = (T)z[k * ld + p];
+        T dz = det_eq6<T>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8]);
+        g[p] = (WT)(T(1) / MUL(T(8), dz));
+    }
+}
+
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// w = r^(-alpha), alpha = L/(2h).  alpha == 2 (L = 4, h = 1): w = 1/(r r),
+// no transcendental.
+__device__ __forceinline__ float pair_weight(float r, float alpha, bool alpha_is_2) {
+    if (alpha_is_2) return fast_rcp(r * r);
+    return exp2f(-alpha * log2f(r));
+}
+__device__ __forceinline__ double pair_weight(double r, double alpha, bool alpha_is_2) {
+    if (alpha_is_2) return 1.0 / (r * r);
+    return exp(-alpha * log(r));
+}
+
+// K3b.  r = D_S^2 / (D_i D_j) with D_S = det(Z_i + Z_j)/8 = (ds g_i)(ds g_j).
+template <typename S, typename T, typename WT>
+__global__ void __launch_bounds__(K3_THREADS)
+k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
+             int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
+             int alpha_is_2, S* __restrict__ out) {
+    extern __shared__ unsigned char smem_raw[];
+    const int HW = K3_TX + 2 * R;        // halo tile width
+    const int HH = K3_TY + 2 * R;        // halo tile height
+    const int HP = HW * HH;              // pixels in the halo tile
+    T* sz = reinterpret_cast<T*>(smem_raw);        // 9 planes of Z (type T)
+    WT* sg = reinterpret_cast<WT*>(sz + 9 * HP);   // 1 plane of g
+
+    const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
+    const int64_t y0 = row_begin + (int64_t)blockIdx.y * K3_TY;
+    // stage the halo (clipped to the slab; out-of-slab cells are never read)
+    for (int q = threadIdx.x; q < HP; q += blockDim.x) {
+        int hy = q / HW, hx = q % HW;
+        int64_t gy = y0 - R + hy, gx = x0 - R + hx;
+        if (gy >= 0 && gy < slab_rows && gx >= 0 && gx < width) {
+            int64_t p = gy * width + gx;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) sz[k * HP + q] = (T)z[k * ld + p];
+            sg[q] = g[p];
+        }
+    }
+    __syncthreads();
+
+    const int tx = threadIdx.x % K3_TX;
+    const int ty0 = (threadIdx.x / K3_TX) * K3_RB;
+    const int64_t gx = x0 + tx;
+    T zi[K3_RB][9];
+    WT gi[K3_RB];
+    double acc[K3_RB];
+    bool live[K3_RB];
+#pragma unroll
+    for (int r = 0; r < K3_RB; ++r) {
+        int64_t gy = y0 + ty0 + r;
+        live[r] = gx < width && gy < row_end;
+        int q = (ty0 + r + R) * HW + (tx + R);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) zi[r][k] = live[r] ? sz[k * HP + q] : T(0);
+        gi[r] = live[r] ? sg[q] : WT(0);
+        acc[r] = 0.0;
+    }
+    const WT alpha = (WT)alpha_d;
+    const bool a2 = alpha_is_2 != 0;
+    // window rows reachable from any of the RB pixels
+    for (int wy = -R; wy <= R + K3_RB - 1; ++wy) {
+        int64_t gyj = y0 + ty0 + wy;
+        if (gyj < 0 || gyj >= slab_rows) continue;
+        int hy = ty0 + wy + R;
+        WT row[K3_RB];
+#pragma unroll
+        for (int r = 0; r < K3_RB; ++r) row[r] = WT(0);
+        for (int wx = -R; wx <= R; ++wx) {
+            int64_t gxj = gx + wx;
+            if (gxj < 0 || gxj >= width) continue;
+            int q = hy * HW + (tx + wx + R);
+            T zj[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) zj[k] = sz[k * HP + q];
+            WT gj = sg[q];
+#pragma unroll
+            for (int r = 0; r < K3_RB; ++r) {
+                int dy = wy - r;
+                if (dy < -R || dy > R || !live[r]) continue;
+                T ds = det_eq6<T>(ADD(zi[r][0], zj[0]), ADD(zi[r][1], zj[1]), ADD(zi[r][2], zj[2]),
+                                  ADD(zi[r][3], zj[3]), ADD(zi[r][4], zj[4]), ADD(zi[r][5], zj[5]),
+                                  ADD(zi[r][6], zj[6]), ADD(zi[r][7], zj[7]), ADD(zi[r][8], zj[8]));
+                WT fds = (WT)ds;
+                WT rr = (fds * gi[r]) * (fds * gj);
+                row[r] += pair_weight(rr, alpha, a2);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < K3_RB; ++r) acc[r] += (double)row[r];
+    }
+#pragma unroll
+    for (int r = 0; r < K3_RB; ++r) {
+        int64_t gy = y0 + ty0 + r;
+        if (live[r]) out[(gy - row_begin) * width + gx] = (S)acc[r];
+    }
+}
+
+template <typename S, typename T, typename WT>
+int launch_window(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
+                  int64_t re, int R, double looks, double h, void* ws, void* outv,
+                  cudaStream_t s) {
+    const S* z = (const S*)zv;
+    WT* g = (WT*)ws;
+    int64_t n = slab_rows * width;
+    k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
+    int HW = K3_TX + 2 * R, HH = K3_TY + 2 * R;
+    size_t smem = (size_t)HW * HH * (9 * sizeof(T) + sizeof(WT));
+    auto kern = k_window_sum<S, T, WT>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
+    double alpha = looks / (2.0 * h);
+    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - rb + K3_TY - 1) / K3_TY));
+    kern<<<grid, K3_THREADS, smem, s>>>(z, ld, width, slab_rows, rb, re, R, g, alpha,
+                                        alpha == 2.0 ? 1 : 0, (S*)outv);
+    return launch_check("polsar_window_distance: launch failed");
+}
+
+// ======================================================= R1: checksums
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+
+template <typename U>
+__global__ void __launch_bounds__(256)
+k_checksum(const U* __restrict__ planes, int64_t n, int64_t ld, int nplanes, int64_t pix_offset,
+           const uint8_t* __restrict__ status, unsigned long long* __restrict__ result) {
+    uint64_t h = 0;
+    unsigned long long c0 = 0, c1 = 0, c2 = 0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key = (uint64_t)(pix_offset + p) * 0x9E3779B97F4A7C15ull;
+        for (int k = 0; k < nplanes; ++k)
+            h += mix64((uint64_t)planes[k * ld + p] ^ (key + (uint64_t)k * 0xD6E8FEB86659FD93ull));
+        if (status) {
+            uint8_t s = status[p];
+            c0 += s == 0;
+            c1 += s == 1;
+            c2 += s == 2;
+        }
+    }
+    // warp reduction, then one atomic per warp (wrapping uint64 sums commute)
+    for (int o = 16; o > 0; o >>= 1) {
+        h += __shfl_down_sync(0xffffffffu, h, o);
+        c0 += __shfl_down_sync(0xffffffffu, c0, o);
+        c1 += __shfl_down_sync(0xffffffffu, c1, o);
+        c2 += __shfl_down_sync(0xffffffffu, c2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(result + 0, (unsigned long long)h);
+        if (status) {
+            atomicAdd(result + 1, c0);
+            atomicAdd(result + 2, c1);
+            atomicAdd(result + 3, c2);
+        }
+    }
+}
+
+}  // namespace
+
+// ============================================================== C-ABI
+extern "C" {
+
+int polsar_inv_det(const void* z, void* out, uint8_t* status, int64_t n, int64_t ld, int dtype,
+                   void* cuda_stream) {
+    return dispatch_inv_det<ALGO_ADJ>(z, out, status, n, ld, dtype, cuda_stream);
+}
+
+int polsar_inv_det_cholesky(const void* z, void* out, uint8_t* status, int64_t n, int64_t ld,
+                            int dtype, void* cuda_stream) {
+    return dispatch_inv_det<ALGO_CHOL>(z, out, status, n, ld, dtype, cuda_stream);
+}
+
+size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int dtype) {
+    if (slab_rows < 0 || width < 0) return 0;
+    // one plane of g_i = 1/(8 det Z_i) in the weight type: fp64 for the F64
+    // modes, fp32 otherwise (rounded up to 256 bytes)
+    size_t es = (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) ? 8 : 4;
+    return (((size_t)(slab_rows * width) * es) + 255) / 256 * 256;
+}
+
+int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
+                           int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
+                           double h, void* workspace, void* out, int dtype, void* cuda_stream) {
+    if (width < 0 || slab_rows < 0) return fail(POLSAR_EINVAL, "negative size");
+    if (out_row_begin < 0 || out_row_end < out_row_begin || out_row_end > slab_rows)
+        return fail(POLSAR_EINVAL, "bad output row range");
+    if (radius < 0 || radius > 32) return fail(POLSAR_EINVAL, "radius out of [0, 32]");
+    if (!(looks > 0) || !(h > 0)) return fail(POLSAR_EINVAL, "looks and h must be > 0");
+    if (ld < slab_rows * width) return fail(POLSAR_EINVAL, "ld < slab_rows*width");
+    if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
+    if (!z || !workspace || !out) return fail(POLSAR_EINVAL, "null pointer");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    switch (dtype) {
+        case POLSAR_F32:
+            return launch_window<float, double, float>(z, ld, width, slab_rows, out_row_begin,
+                                                       out_row_end, radius, looks, h, workspace, out, s);
+        case POLSAR_F64:
+        case POLSAR_F64_PLAIN:
+            return launch_window<double, double, double>(z, ld, width, slab_rows, out_row_begin,
+                                                         out_row_end, radius, looks, h, workspace, out, s);
+        case POLSAR_F32_PLAIN:
+            return launch_window<float, float, float>(z, ld, width, slab_rows, out_row_begin,
+                                                      out_row_end, radius, looks, h, workspace, out, s);
+        default: return fail(POLSAR_EINVAL, "bad dtype");
+    }
+}
+
+int polsar_checksum(const void* planes, int64_t n, int64_t ld, int nplanes, int dtype,
+                    int64_t pix_offset, const uint8_t* status, uint64_t* result, void* cuda_stream) {
+    if (n < 0 || ld < n || nplanes < 0 || !result) return fail(POLSAR_EINVAL, "bad checksum args");
+    if (n == 0) return POLSAR_OK;
+    if (nplanes > 0 && !planes) return fail(POLSAR_EINVAL, "null planes");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    int grid = grid_for(n, 256);
+    if (dtype == POLSAR_F32 || dtype == POLSAR_F32_PLAIN)
+        k_checksum<uint32_t><<<grid, 256, 0, s>>>((const uint32_t*)planes, n, ld, nplanes, pix_offset,
+                                                  status, (unsigned long long*)result);
+    else if (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN)
+        k_checksum<uint64_t><<<grid, 256, 0, s>>>((const uint64_t*)planes, n, ld, nplanes, pix_offset,
+                                                  status, (unsigned long long*)result);
+    else
+        return fail(POLSAR_EINVAL, "bad dtype");
+    return launch_check("polsar_checksum: launch failed");
+}
+
+int64_t polsar_host_chunk_pixels(size_t ws_bytes, int dtype) {
+    size_t es = (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) ? 8 : 4;
+    // 3 slots x (9 in + 11 out planes + 1 status byte) per pixel, chunk a
+    // multiple of 64 pixels so every device plane stays 256-byte aligned
+    size_t per = 3 * (20 * es + 1);
+    int64_t c = (int64_t)(ws_bytes / per);
+    return (c / 64) * 64;
+}
+
+int polsar_inv_det_host(const void* z_host, void* out_host, uint8_t* status_host, int64_t n,
+                        int64_t ld_host, int dtype, int algo, void* dev_ws, size_t ws_bytes,
+                        void* stream_h2d, void* stream_compute, void* stream_d2h) {
+    if (n < 0 || ld_host < n) return fail(POLSAR_EINVAL, "bad n / ld_host");
+    if (n == 0) return POLSAR_OK;
+    if (!z_host || !out_host || !dev_ws) return fail(POLSAR_EINVAL, "null pointer");
+    if ((uintptr_t)dev_ws % 256) return fail(POLSAR_EINVAL, "dev_ws must be 256-byte aligned");
+    if (algo != 0 && algo != 1) return fail(POLSAR_EINVAL, "bad algo");
+    if (dtype < POLSAR_F32 || dtype > POLSAR_F64_PLAIN) return fail(POLSAR_EINVAL, "bad dtype");
+    if (!stream_h2d || !stream_compute || !stream_d2h || stream_h2d == stream_compute ||
+        stream_h2d == stream_d2h || stream_compute == stream_d2h)
+        return fail(POLSAR_EINVAL, "three distinct non-null streams required");
+    const size_t es = (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) ? 8 : 4;
+    const int64_t chunk = polsar_host_chunk_pixels(ws_bytes, dtype);
+    if (chunk <= 0) return fail(POLSAR_EINVAL, "workspace too small");
+    cudaStream_t sh = (cudaStream_t)stream_h2d, sc = (cudaStream_t)stream_compute,
+                 sd = (cudaStream_t)stream_d2h;
+    // slot layout: [9 in planes][11 out planes][status], each plane `chunk` elements
+    const size_t slot_bytes = (size_t)chunk * (20 * es + 1);
+    cudaEvent_t ev_in[3], ev_k[3], ev_out[3];
+    for (int i = 0; i < 3; ++i) {
+        cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_k[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming);
+    }
+    int rc = POLSAR_OK;
+    const int64_t n_chunks = (n + chunk - 1) / chunk;
+    for (int64_t c = 0; c < n_chunks && rc == POLSAR_OK; ++c) {
+        const int slot = (int)(c % 3);
+        const int64_t p0 = c * chunk;
+        const int64_t m = (n - p0) < chunk ? (n - p0) : chunk;
+        unsigned char* base = (unsigned char*)dev_ws + slot * slot_bytes;
+        unsigned char* din = base;
+        unsigned char* dout = base + (size_t)9 * chunk * es;
+        uint8_t* dst = (uint8_t*)(base + (size_t)20 * chunk * es);
+        if (c >= 3) cudaStreamWaitEvent(sh, ev_out[slot], 0);  // slot drained by its D2H
+        if (cudaMemcpy2DAsync(din, chunk * es, (const unsigned char*)z_host + p0 * es, ld_host * es,
+                              m * es, 9, cudaMemcpyHostToDevice, sh) != cudaSuccess) {
+            rc = fail(POLSAR_ECUDA, "polsar_inv_det_host: H2D copy failed");
+            break;
+        }
+        cudaEventRecord(ev_in[slot], sh);
+        cudaStreamWaitEvent(sc, ev_in[slot], 0);
+        rc = (algo == 0 ? polsar_inv_det : polsar_inv_det_cholesky)(
+            din, dout, status_host ? dst : nullptr, m, chunk, dtype, sc);
+        if (rc != POLSAR_OK) break;
+        cudaEventRecord(ev_k[slot], sc);
+        cudaStreamWaitEvent(sd, ev_k[slot], 0);
+        if (cudaMemcpy2DAsync((unsigned char*)out_host + p0 * es, ld_host * es, dout, chunk * es,
+                              m * es, 11, cudaMemcpyDeviceToHost, sd) != cudaSuccess) {
+            rc = fail(POLSAR_ECUDA, "polsar_inv_det_host: D2H copy failed");
+            break;
+        }
+        if (status_host &&
+            cudaMemcpyAsync(status_host + p0, dst, m, cudaMemcpyDeviceToHost, sd) != cudaSuccess) {
+            rc = fail(POLSAR_ECUDA, "polsar_inv_det_host: D2H status copy failed");
+            break;
+        }
+        cudaEventRecord(ev_out[slot], sd);
+    }
+    if (cudaStreamSynchronize(sd) != cudaSuccess && rc == POLSAR_OK)
+        rc = fail(POLSAR_ECUDA, "polsar_inv_det_host: stream error");
+    for (int i = 0; i < 3; ++i) {
+        cudaEventDestroy(ev_in[i]);
+        cudaEventDestroy(ev_k[i]);
+        cudaEventDestroy(ev_out[i]);
+    }
+    return rc;
+}
+
+const char* polsar_last_error(void) { return g_last_error; }
+
+int polsar_version(void) { return 0x000100; }
+
+}  // extern "C"

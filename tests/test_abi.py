@@ -1,0 +1,89 @@
+"""Host-side checks of the C-ABI (no GPU needed): the libraries build for
+sm_100a, load, export every symbol the headers declare, and validate
+arguments synchronously (EINVAL paths never touch the device)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_1807_08084_b200 import _build, _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared(header):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\*\s]+?\b(polsar_\w+)\s*\(", src, flags=re.M))
+                  - {"polsar_gen_threshold"})
+
+
+def exported(so):
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True,
+                         check=True).stdout
+    return {line.split()[-1] for line in out.splitlines() if line.strip()}
+
+
+def test_libpolsar_exports_every_declared_symbol():
+    so = _build.build_target("libpolsar")
+    syms = exported(so)
+    names = declared("polsar.h")
+    assert set(_lib.SIGNATURES) == set(names)
+    for name in names:
+        assert name in syms, name
+
+
+def test_generator_exports():
+    gpu = exported(_build.build_target("libpolsar_gen"))
+    cpu = exported(_build.build_target("libpolsar_gen_cpu"))
+    names = declared("polsar_gen.h")
+    assert "polsar_gen_wishart" in names
+    assert "polsar_gen_wishart" in gpu
+    assert {"polsar_gen_wishart_cpu", "polsar_gen_wishart_pixels_cpu"} <= cpu
+
+
+def test_sm100a_cubin_only():
+    so = _build.build_target("libpolsar")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True,
+                         text=True, check=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+def test_loads_and_validates_without_gpu():
+    lib = _lib.lib()
+    assert lib.polsar_version() >= 0x000100
+    # argument errors are reported synchronously, before any CUDA call
+    assert lib.polsar_inv_det(None, None, None, -1, 0, 0, None) == 1
+    assert lib.polsar_inv_det(None, None, None, 10, 5, 0, None) == 1
+    assert b"ld" in lib.polsar_last_error()
+    assert lib.polsar_inv_det(None, None, None, 0, 0, 0, None) == 0  # n == 0 no-op
+    assert lib.polsar_inv_det_cholesky(None, None, None, 4, 4, 9, None) == 1
+    assert lib.polsar_window_distance(None, 0, 4, 4, 0, 5, 11, 4.0, 1.0, None, None, 0, None) == 1
+    assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 40, 4.0, 1.0, None, None, 0, None) == 1
+    assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 3, 0.0, 1.0, None, None, 0, None) == 1
+    assert lib.polsar_checksum(None, 5, 2, 1, 0, 0, None, None, None) == 1
+    assert lib.polsar_inv_det_host(None, None, None, 5, 5, 0, 0, None, 0, None, None, None) == 1
+    assert lib.polsar_window_workspace_bytes(2048, 2048, 0) >= 2048 * 2048 * 4
+    assert lib.polsar_host_chunk_pixels(3 << 30, 0) % 64 == 0
+
+
+def test_binding_refuses_cpu_tensors():
+    torch = pytest.importorskip("torch")
+    import paper_1807_08084_b200 as P
+    z = torch.zeros((9, 4))
+    with pytest.raises(P.PolsarError):
+        P.polsar_inv_det(z, torch.zeros((11, 4)))
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1807_08084_b200")
+    for dp, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".c", ".h")):
+                txt = open(os.path.join(dp, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, flags=re.M), f
+                assert not re.search(r'#include\s+[<"][^>"]*oracle', txt), f
+                assert "liboracle" not in txt, f

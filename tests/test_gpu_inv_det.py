@@ -1,0 +1,207 @@
+"""Parity of K1 (Alg. 2) and K2 (Alg. 1) against the CPU oracle, through the
+C-ABI (via the thin binding), on seeded synthetic inputs.
+
+Tolerance (BASELINE north_star): max relative error <= 1e-12 (fp64 storage)
+and <= 2e-5 (fp32 storage) on the inverse (normwise per pixel, R-10), det and
+det^-1, over pixels with kappa_2 <= 1e4.  The *_PLAIN modes (Alg. 2 exactly
+as printed, in the storage precision) are reported, not asserted.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1807_08084_b200 as P
+from paper_1807_08084_b200 import configs, wishart
+from tests._metrics import TOL, entrywise, errors, worst
+
+pytestmark = pytest.mark.gpu
+THREADS = len(os.sched_getaffinity(0))
+ALGOS = ["adjugate", "cholesky"]
+
+
+def run(z, algo, plain=False):
+    out, st = P.inv_det(z, algo=algo, plain=plain)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), st.cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def c1(cuda):
+    cfg = configs.get("c1")
+    z = wishart.generate(cfg, device=cuda)
+    zh = z.cpu().numpy()
+    return z, zh, oracle.inv_det(zh), oracle.kappa2(zh)
+
+
+@pytest.fixture(scope="module")
+def c2(cuda):
+    cfg = configs.get("c2")
+    z = wishart.generate(cfg, device=cuda)
+    zh = z.cpu().numpy()
+    return z, zh, oracle.inv_det_threaded(zh, THREADS), oracle.kappa2(zh)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_c1_fp64_parity(c1, algo):
+    z, zh, ref, k = c1
+    got, st = run(z, algo)
+    mask = k <= 1e4
+    assert mask.mean() > 0.99
+    assert worst(got, ref, mask) <= TOL["float64"]
+    assert np.all(st == 0)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_c2_fp32_parity(c2, algo):
+    z, zh, ref, k = c2
+    got, st = run(z, algo)
+    mask = k <= 1e4
+    assert worst(got, ref, mask) <= TOL["float32"]
+    # fp32 storage with fp64 arithmetic: every complex entry is within a few
+    # fp32 roundings of the oracle, not only normwise
+    assert entrywise(got, ref)[mask].max() <= 4 * 2.0 ** -24
+    assert np.all(st == 0)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_plain_modes_reported(c1, c2, algo, capsys):
+    for name, (z, zh, ref, k) in (("c1", c1), ("c2", c2)):
+        got, _ = run(z, algo, plain=True)
+        mask = k <= 1e4
+        e = worst(got, ref, mask)
+        with capsys.disabled():
+            print(f"\n[report] {algo} PLAIN {name} {z.dtype}: max rel err {e:.3e} (kappa<=1e4)")
+        assert np.isfinite(e)
+
+
+def test_golden_matrix_catches_l21(cuda):
+    # PAPER.md:298 prints l21 = (e - l10 conj(l20)) v1; with it c_i = (1-i)/2, e_i = +i.
+    z = torch.tensor([2, 1, 1, 0, 0, 3, 0, 1, 1], dtype=torch.float64, device=cuda).reshape(9, 1)
+    for algo in ALGOS:
+        got, st = run(z, algo)
+        ref = np.array([1, -0.5, -0.5, -0.5, 0.5, 1, 0, -1, 2, 2, 0.5])
+        np.testing.assert_allclose(got[:, 0], ref, rtol=0, atol=4e-16)
+        assert st[0] == 0
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("algo", ALGOS)
+def test_ragged_and_misaligned_bit_identical(cuda, dt, algo):
+    """Scalar tail / misaligned planes give the same bits as the vector body."""
+    cfg = configs.get("c2").scaled(8, 1000)
+    z = wishart.generate(cfg, device=cuda).to(dt)
+    full, st_full = run(z, algo)
+    fn = P.polsar_inv_det if algo == "adjugate" else P.polsar_inv_det_cholesky
+    fn(z[:, :1], torch.empty((11, 1), dtype=dt, device=cuda), None, n=0)  # n == 0 no-op
+    for n in (1, 3, 5, 7, 1023, 4097, 7990):
+        for off in (0, 1, 3):
+            for pad in (0, 5):
+                ld = n + pad
+                zc = torch.empty((9, ld), dtype=dt, device=cuda)
+                zc[:, :n].copy_(z[:, off:off + n])
+                out = torch.full((11, ld), float("nan"), dtype=dt, device=cuda)
+                st = torch.full((n,), 255, dtype=torch.uint8, device=cuda)
+                fn(zc[:, :n], out[:, :n], st, n=n)
+                torch.cuda.synchronize()
+                got = out[:, :n].cpu().numpy()
+                assert np.array_equal(got.view(np.uint8), full[:, off:off + n].copy().view(np.uint8))
+                assert np.array_equal(st.cpu().numpy(), st_full[off:off + n])
+
+
+@pytest.mark.parametrize("m", [1, -3, 5])
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_power_of_two_metamorphic_bit_exact(c2, dt, m):
+    z = c2[0].to(dt)
+    k = 2.0 ** m
+    a, _ = run(z, "adjugate")
+    b, _ = run(z * k, "adjugate")
+    assert np.array_equal(b[:9], a[:9] / np.asarray(k, a.dtype))
+    assert np.array_equal(b[9], a[9] * np.asarray(k ** 3, a.dtype))
+    assert np.array_equal(b[10], a[10] / np.asarray(k ** 3, a.dtype))
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_det_times_reciprocal(c2, dt):
+    z = c2[0].to(dt)
+    got, st = run(z, "adjugate")
+    if dt == torch.float64:
+        # t = RN(1/det) exactly: |det t - 1| <= u
+        prod = got[9] * got[10]
+        assert np.all(np.abs(prod - 1) <= 2.0 ** -52)
+    else:
+        prod = got[9].astype(np.float64) * got[10].astype(np.float64)
+        assert np.all(np.abs(prod - 1) <= 2 * 2.0 ** -24)
+
+
+@pytest.mark.parametrize("looks", [1, 2])
+def test_rank_deficient_flagged_singular(cuda, looks):
+    base = configs.get("c2").scaled(16, 1000)
+    cfg = configs.Config(**{**base.__dict__, "looks": looks, "name": f"L{looks}"})
+    for dt in (torch.float32, torch.float64):
+        z = wishart.generate(cfg, device=cuda).to(dt)
+        _, st = run(z, "adjugate")
+        assert np.all(st == 1), (looks, dt, np.bincount(st))
+
+
+def test_looks_ge_3_not_flagged(cuda):
+    base = configs.get("c2").scaled(16, 1000)
+    cfg = configs.Config(**{**base.__dict__, "looks": 3, "name": "L3"})
+    z = wishart.generate(cfg, device=cuda)
+    _, st = run(z, "adjugate")
+    assert np.mean(st == 0) > 0.999
+
+
+def test_not_pd_and_nonfinite_status(cuda):
+    # indefinite, negative diagonal, NaN input
+    cols = [[1, 2, 0, 0, 0, 1, 0, 0, 1],      # |b|^2 > a d: indefinite
+            [-1, 0, 0, 0, 0, 1, 0, 0, 1],     # a < 0
+            [float("nan"), 0, 0, 0, 0, 1, 0, 0, 1],
+            [1, 0, 0, 0, 0, 1, 0, 0, 1]]
+    z = torch.tensor(cols, dtype=torch.float64, device=cuda).T.contiguous()
+    _, st_adj = run(z, "adjugate")
+    _, st_chol = run(z, "cholesky")
+    assert list(st_adj) == [1, 1, 1, 0]
+    assert list(st_chol) == [2, 2, 2, 0]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_cross_method_agreement(c1, algo):
+    z, zh, ref, k = c1
+    a, _ = run(z, "adjugate")
+    b, _ = run(z, "cholesky")
+    mask = k <= 1e6
+    inv, det, idet = errors(a, b.astype(np.float64))
+    assert inv[mask].max() <= 1e-9 and det[mask].max() <= 1e-10
+
+
+def test_checksum_split_invariance(c2):
+    z = c2[0]
+    out, st = P.inv_det(z)
+    n = z.shape[1]
+    full = P.polsar_checksum(out, n, 11, 0, st)
+    parts = torch.zeros(4, dtype=torch.int64, device=z.device)
+    for lo, hi in ((0, 1000), (1000, 777777), (777777, n)):
+        P.polsar_checksum(out[:, lo:], hi - lo, 11, lo, st[lo:], result=parts)
+    torch.cuda.synchronize()
+    assert torch.equal(full, parts)
+    assert int(full[1]) == n
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("algo", [0, 1])
+def test_host_pipeline_matches_device(c2, dt, algo):
+    z = c2[0][:, :300_001].to(dt).contiguous()
+    n = z.shape[1]
+    dev_out, dev_st = P.inv_det(z, algo="adjugate" if algo == 0 else "cholesky")
+    zh = z.cpu().pin_memory()
+    oh = torch.empty((11, n), dtype=dt).pin_memory()
+    sh = torch.empty(n, dtype=torch.uint8).pin_memory()
+    ws = torch.empty(4 << 20, dtype=torch.uint8, device=z.device)  # small: many chunks
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    P.polsar_inv_det_host(zh, oh, sh, ws, streams, algo=algo)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, dev_out.cpu())
+    assert torch.equal(sh, dev_st.cpu())

@@ -1,0 +1,89 @@
+"""K3 (search-window log-det distance sum, BASELINE configs[4]) against the
+long-double window oracle, plus closed forms and slab-consistency."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1807_08084_b200 as P
+from paper_1807_08084_b200 import configs, wishart
+
+pytestmark = pytest.mark.gpu
+THREADS = len(os.sched_getaffinity(0))
+TOL = {torch.float32: 2e-5, torch.float64: 1e-12}
+
+
+def clipped_counts(h, w, r):
+    ys, xs = np.divmod(np.arange(h * w), w)
+    ny = np.minimum(h - 1, ys + r) - np.maximum(0, ys - r) + 1
+    nx = np.minimum(w - 1, xs + r) - np.maximum(0, xs - r) + 1
+    return (ny * nx).astype(np.float64)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 53), 3), ((20, 70), 0), ((150, 33), 11)])
+def test_window_parity(cuda, dt, shape, radius):
+    h, w = shape
+    cfg = configs.get("c5").scaled(h, w)
+    z = wishart.generate(cfg, device=cuda).to(dt)
+    got = P.window_distance(z, h, w, radius=radius, looks=4.0, h=1.0).cpu().numpy()
+    zh = z.cpu().numpy()
+    ref = oracle.window_threaded(zh, h, w, radius, 4.0, 1.0, np.arange(h * w), THREADS)
+    rel = np.abs(got - ref) / ref
+    assert rel.max() <= TOL[dt], rel.max()
+    assert np.all(got >= 1 - 1e-6)
+
+
+@pytest.mark.parametrize("looks,hh", [(8.0, 1.0), (4.0, 2.5), (3.0, 1.0)])
+def test_window_general_exponent(cuda, looks, hh):
+    h, w, r = 40, 45, 5
+    cfg = configs.get("c5").scaled(h, w)
+    z = wishart.generate(cfg, device=cuda)
+    got = P.window_distance(z, h, w, radius=r, looks=looks, h=hh).cpu().numpy()
+    ref = oracle.window_threaded(z.cpu().numpy(), h, w, r, looks, hh, np.arange(h * w), THREADS)
+    assert (np.abs(got - ref) / ref).max() <= 2e-5
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_window_constant_image(cuda, dt):
+    h, w, r = 70, 90, 11
+    cfg = configs.get("c5").scaled(1, 1)
+    z1 = wishart.generate(cfg, device=cuda).to(dt)
+    z = z1.repeat(1, h * w).contiguous()
+    got = P.window_distance(z, h, w, radius=r).cpu().numpy()
+    ref = clipped_counts(h, w, r)
+    assert np.allclose(got, ref, rtol=TOL[dt], atol=0)
+
+
+def test_window_slab_consistency(cuda):
+    """Rows computed from a halo slab equal the same rows of a whole-image
+    pass bit for bit (the multi-GPU decomposition of R-12)."""
+    h, w, r = 200, 64, 11
+    cfg = configs.get("c5").scaled(h, w)
+    z = wishart.generate(cfg, device=cuda)
+    full = P.window_distance(z, h, w, radius=r)
+    for r0, r1 in ((0, 50), (50, 123), (123, 200)):
+        s0, s1 = max(0, r0 - r), min(h, r1 + r)
+        slab = wishart.generate(cfg, s0, s1, device=cuda)
+        part = P.window_distance(slab, s1 - s0, w, radius=r, row_begin=r0 - s0, row_end=r1 - s0)
+        assert torch.equal(part, full[r0 * w:r1 * w])
+
+
+def test_window_c5_sampled(cuda):
+    """Full 2048^2 c5 at R = 11 in the bench's launch configuration; a
+    sample of pixels (corners, edges, tile seams, random) against the oracle."""
+    cfg = configs.get("c5")
+    h, w = cfg.height, cfg.width
+    z = wishart.generate(cfg, device=cuda)
+    got = P.window_distance(z, h, w, radius=cfg.radius, looks=cfg.looks, h=cfg.h).cpu().numpy()
+    rng = np.random.default_rng(0)
+    idx = np.concatenate([[0, w - 1, (h - 1) * w, h * w - 1, 63 * w + 64, 64 * w + 63],
+                          rng.integers(0, h * w, 3000)])
+    # the oracle needs only the window of each sampled pixel: regenerate on the host
+    zh = z.cpu().numpy()
+    ref = oracle.window_threaded(zh, h, w, cfg.radius, cfg.looks, cfg.h, idx, THREADS)
+    rel = np.abs(got[idx] - ref) / ref
+    assert rel.max() <= 2e-5, rel.max()
+    assert np.all(np.isfinite(got)) and got.min() >= 1 - 1e-6 and got.max() <= 529 + 1e-3
