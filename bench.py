@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-extras", action="store_true", help="skip the K2 / K3 side measurements")
     p.add_argument("--no-status", action="store_true")
     p.add_argument("--verify", action="store_true", help="sampled oracle check after timing")
+    p.add_argument("--rows", type=int, default=0,
+                   help="override rows per GPU (profiling runs only; not a bench line)")
     return p.parse_args()
 
 
@@ -138,11 +140,10 @@ def setup_dist(args):
 
 
 def rows_for(rank, world, cfg, scaling):
+    from paper_1807_08084_b200 import dist as pdist
     if scaling == "weak":
-        H = cfg.height * world
-        return H, rank * cfg.height, (rank + 1) * cfg.height
-    H = cfg.height
-    return H, (rank * H) // world, ((rank + 1) * H) // world
+        return pdist.weak_rows(cfg.height, world, rank)
+    return (cfg.height,) + pdist.shard_rows(cfg.height, world, rank)
 
 
 def bytes_per_matrix(esz, status):
@@ -210,6 +211,8 @@ def run_ours(args):
     cfg = configs.get(args.config)
     if cfg.radius:
         raise SystemExit("window configs are measured as an extra; pick c1..c4 for --config")
+    if args.rows:
+        cfg = cfg.scaled(args.rows)
     H, r0, r1 = rows_for(rank, world, cfg, args.scaling)
     n = (r1 - r0) * cfg.width
     tdt = torch.float32 if cfg.dtype == "float32" else torch.float64
@@ -254,15 +257,6 @@ def run_ours(args):
         dist.barrier()
     per_step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_local = sum(per_step_ms) / 1e3  # kernel-only time of the K timed steps
-    t_max = t_local
-    if world > 1:
-        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-    total = n * world
-    value = total * args.steps / t_max
-    ms_per_step = t_max / args.steps * 1e3
-
     # roofline of the (only) kernel of the step
     bpm = bytes_per_matrix(esz, status is not None)
     achieved = n * bpm / (t_local / args.steps) / 1e9
@@ -270,15 +264,19 @@ def run_ours(args):
     key = f"{cfg.name}:{args.algo}:{'plain' if args.plain else 'default'}"
     traffic = read_traffic(key)
 
-    # multi-GPU verification reduction (outside the timed region): checksum
-    # of all outputs + status counts, NCCL all_reduce (SUM wraps like uint64)
+    # SURVEY §8(a) row D, after the timed region: order-independent checksum
+    # of all outputs + status counts (NCCL SUM; int64 wraps like uint64) and
+    # the kernel time (NCCL MAX over ranks)
+    from paper_1807_08084_b200 import dist as pdist
     res = P.polsar_checksum(out, n, 11, r0 * cfg.width, status, stream=stream)
     stream.synchronize()
-    if world > 1:
-        dist.all_reduce(res, op=dist.ReduceOp.SUM)
+    res, t_max = pdist.reduce_results(res, t_local)
     checksum = int(res[0].item()) & 0xFFFFFFFFFFFFFFFF
     counts = [int(x) for x in res[1:].tolist()]
 
+    total = n * world
+    value = total * args.steps / t_max
+    ms_per_step = t_max / args.steps * 1e3
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
