@@ -107,7 +107,8 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int dtype
  *               at the slab edge equals clipping at the image edge.
  *   out_row_begin, out_row_end : slab rows whose W is written (0 <= b <= e
  *               <= slab_rows); out receives (e - b) x width values, row-major.
- *   radius R (>= 0, <= 32), looks L (> 0), h (> 0).
+ *   radius R (>= 0, <= 16; the paper's 23x23 window is R = 11), looks L (> 0),
+ *               h (> 0).
  *   workspace : device, polsar_window_workspace_bytes(slab_rows, width, dtype)
  *   dtype     : POLSAR_F32 (fp32 storage, fp64 pair determinant, fp32
  *               weight) or POLSAR_F64 (fp64 throughout), or the _PLAIN

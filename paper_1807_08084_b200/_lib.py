@@ -43,8 +43,12 @@ def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
         path = _build.TARGETS["libpolsar"]["out"]
+        override = os.environ.get("POLSAR_LIB_OVERRIDE")  # development A/B builds only
+        if override:
+            path = override
         try:
-            _build.build_target("libpolsar")
+            if not override:
+                _build.build_target("libpolsar")
         except Exception as e:  # toolchain missing: only an existing .so will do
             if not os.path.exists(path):
                 raise PolsarError(f"libpolsar.so is not built and cannot be built: {e}") from e

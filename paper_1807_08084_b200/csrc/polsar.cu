@@ -473,18 +473,23 @@ int dispatch_inv_det(const void* z, void* out, uint8_t* status, int64_t n, int64
 }
 
 // ==================================================== K3: window distance
-// K3a: per-pixel det Z_i (Eq. 6) into the workspace (fp64).
-// K3b: one CTA per TY x TX output tile; the (TY+2R) x (TX+2R) halo of Z and
-// D is staged in shared memory as fp64 planes; each thread owns RB
-// vertically adjacent output pixels and walks the window, reusing every
-// staged Z_j for all of its pixels within reach.  Per pair (R-12, BASELINE
-// configs[4]):  S = Z_i + Z_j  (exact in fp64 for fp32 storage),
-//   D_S = det(S)/8 = det((Z_i+Z_j)/2) by Eq. 6 (only a_c, b_c, c_c needed),
-//   r = (D_S / D_i)(D_S / D_j),  exp(-d_ij/h) = r^(-L/(2h)).
-constexpr int K3_TX = 32;
-constexpr int K3_TY = 16;
-constexpr int K3_RB = 2;                          // output rows per thread
-constexpr int K3_THREADS = K3_TX * K3_TY / K3_RB;  // 256
+// K3a: per-pixel g_i = 1/(8 det Z_i) (det by Eq. 6) into the workspace.
+// K3b: one CTA per TY x TX output tile; the (TY+2R) x (TX+2R) halo of Z (9
+// planes, type T) and g (1 plane) is staged in shared memory once.  Each
+// thread owns RB vertically adjacent output pixels of one column and walks
+// the window's columns; every staged Z_j it loads is paired with all of its
+// RB pixels that reach it (RB-fold reuse of each shared-memory load, RB
+// independent dependency chains for the FP64 pipe).  Per pair (R-12,
+// BASELINE configs[4]):
+//   S = Z_i + Z_j            (9 adds; exact in fp64 for fp32 storage)
+//   ds = det(S) by Eq. 6     (only a_c, b_c, c_c needed: 20 fp64 ops)
+//   r = (ds g_i)(ds g_j) = D_S^2 / (D_i D_j),  D_S = det((Z_i+Z_j)/2)
+//   exp(-d_ij/h) = r^(-L/(2h))   (L/(2h) = 2: 1/(r r), no transcendental)
+// Rows of the window that reach all RB pixels run branch-free; the RB-1 rows
+// at each vertical end take a warp-uniform branch per pixel.  Columns outside
+// the image read zero-filled cells and are masked by a select.
+constexpr int K3_TX = 32;  // tile width; tile height TY in {32, 16, 8} (the largest
+                           // whose halo fits in shared memory); K3_RB output rows per thread
 
 template <typename T>
 __device__ __forceinline__ T det_eq6(T a, T br, T bi, T cr, T ci, T d, T er, T ei, T f) {
@@ -527,9 +532,27 @@ __device__ __forceinline__ double pair_weight(double r, double alpha, bool alpha
     return exp(-alpha * log(r));
 }
 
+template <typename T, typename WT>
+__device__ __forceinline__ WT pair_w(const T* zi, WT gi, const T* zj, WT gj, WT alpha, bool a2) {
+    T ds = det_eq6<T>(ADD(zi[0], zj[0]), ADD(zi[1], zj[1]), ADD(zi[2], zj[2]), ADD(zi[3], zj[3]),
+                      ADD(zi[4], zj[4]), ADD(zi[5], zj[5]), ADD(zi[6], zj[6]), ADD(zi[7], zj[7]),
+                      ADD(zi[8], zj[8]));
+    WT fds = (WT)ds;
+    WT rr = (fds * gi) * (fds * gj);
+    return pair_weight(rr, alpha, a2);
+}
+
+#ifndef POLSAR_K3_RB
+#define POLSAR_K3_RB 2
+#endif
+template <int TY>
+struct K3_RB_FOR {
+    static constexpr int v = (TY >= 16) ? POLSAR_K3_RB : 4;
+};
+
 // K3b.  r = D_S^2 / (D_i D_j) with D_S = det(Z_i + Z_j)/8 = (ds g_i)(ds g_j).
-template <typename S, typename T, typename WT>
-__global__ void __launch_bounds__(K3_THREADS)
+template <typename S, typename T, typename WT, int K3_TY, int K3_RB>
+__global__ void __launch_bounds__(K3_TX * K3_TY / K3_RB, 1)
 k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
              int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
              int alpha_is_2, S* __restrict__ out) {
@@ -542,16 +565,15 @@ k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
 
     const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
     const int64_t y0 = row_begin + (int64_t)blockIdx.y * K3_TY;
-    // stage the halo (clipped to the slab; out-of-slab cells are never read)
+    // stage the halo; cells outside the slab are zero-filled (masked later)
     for (int q = threadIdx.x; q < HP; q += blockDim.x) {
         int hy = q / HW, hx = q % HW;
         int64_t gy = y0 - R + hy, gx = x0 - R + hx;
-        if (gy >= 0 && gy < slab_rows && gx >= 0 && gx < width) {
-            int64_t p = gy * width + gx;
+        bool in = gy >= 0 && gy < slab_rows && gx >= 0 && gx < width;
+        int64_t p = in ? gy * width + gx : 0;
 #pragma unroll
-            for (int k = 0; k < 9; ++k) sz[k * HP + q] = (T)z[k * ld + p];
-            sg[q] = g[p];
-        }
+        for (int k = 0; k < 9; ++k) sz[k * HP + q] = in ? (T)z[k * ld + p] : T(0);
+        sg[q] = in ? g[p] : WT(0);
     }
     __syncthreads();
 
@@ -561,45 +583,70 @@ k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
     T zi[K3_RB][9];
     WT gi[K3_RB];
     double acc[K3_RB];
-    bool live[K3_RB];
 #pragma unroll
     for (int r = 0; r < K3_RB; ++r) {
-        int64_t gy = y0 + ty0 + r;
-        live[r] = gx < width && gy < row_end;
         int q = (ty0 + r + R) * HW + (tx + R);
 #pragma unroll
-        for (int k = 0; k < 9; ++k) zi[r][k] = live[r] ? sz[k * HP + q] : T(0);
-        gi[r] = live[r] ? sg[q] : WT(0);
+        for (int k = 0; k < 9; ++k) zi[r][k] = sz[k * HP + q];
+        gi[r] = sg[q];
         acc[r] = 0.0;
     }
     const WT alpha = (WT)alpha_d;
     const bool a2 = alpha_is_2 != 0;
-    // window rows reachable from any of the RB pixels
+    // the CTA's window columns all lie inside the image: no column masks
+    const bool interior_x = (x0 - R >= 0) && (x0 + K3_TX + R <= width);
+
     for (int wy = -R; wy <= R + K3_RB - 1; ++wy) {
-        int64_t gyj = y0 + ty0 + wy;
-        if (gyj < 0 || gyj >= slab_rows) continue;
-        int hy = ty0 + wy + R;
+        const int64_t gyj = y0 + ty0 + wy;
+        if (gyj < 0 || gyj >= slab_rows) continue;  // warp-uniform
+        const int hy = ty0 + wy + R;
+        const T* rowz = sz + hy * HW + tx + R;
+        const WT* rowg = sg + hy * HW + tx + R;
         WT row[K3_RB];
 #pragma unroll
         for (int r = 0; r < K3_RB; ++r) row[r] = WT(0);
-        for (int wx = -R; wx <= R; ++wx) {
-            int64_t gxj = gx + wx;
-            if (gxj < 0 || gxj >= width) continue;
-            int q = hy * HW + (tx + wx + R);
-            T zj[9];
+        if ((wy >= K3_RB - 1 - R) && (wy <= R)) {
+            // this window row reaches every owned pixel: straight-line RB pairs
+            if (interior_x) {
+#pragma unroll 2
+                for (int wx = -R; wx <= R; ++wx) {
+                    T zj[9];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) zj[k] = sz[k * HP + q];
-            WT gj = sg[q];
+                    for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
+                    const WT gj = rowg[wx];
 #pragma unroll
-            for (int r = 0; r < K3_RB; ++r) {
-                int dy = wy - r;
-                if (dy < -R || dy > R || !live[r]) continue;
-                T ds = det_eq6<T>(ADD(zi[r][0], zj[0]), ADD(zi[r][1], zj[1]), ADD(zi[r][2], zj[2]),
-                                  ADD(zi[r][3], zj[3]), ADD(zi[r][4], zj[4]), ADD(zi[r][5], zj[5]),
-                                  ADD(zi[r][6], zj[6]), ADD(zi[r][7], zj[7]), ADD(zi[r][8], zj[8]));
-                WT fds = (WT)ds;
-                WT rr = (fds * gi[r]) * (fds * gj);
-                row[r] += pair_weight(rr, alpha, a2);
+                    for (int r = 0; r < K3_RB; ++r) row[r] += pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
+                }
+            } else {
+                for (int wx = -R; wx <= R; ++wx) {
+                    T zj[9];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
+                    const WT gj = rowg[wx];
+                    const bool colok = gx + wx >= 0 && gx + wx < width;
+#pragma unroll
+                    for (int r = 0; r < K3_RB; ++r) {
+                        WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
+                        row[r] += colok ? w : WT(0);
+                    }
+                }
+            }
+        } else {
+            // one of the RB-1 rows at either end: only some owned pixels reach it
+            for (int wx = -R; wx <= R; ++wx) {
+                T zj[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
+                const WT gj = rowg[wx];
+                const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+#pragma unroll
+                for (int r = 0; r < K3_RB; ++r) {
+                    const int dy = wy - r;
+                    if (dy >= -R && dy <= R) {  // warp-uniform
+                        WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
+                        row[r] += colok ? w : WT(0);
+                    }
+                }
             }
         }
 #pragma unroll
@@ -607,9 +654,31 @@ k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
     }
 #pragma unroll
     for (int r = 0; r < K3_RB; ++r) {
-        int64_t gy = y0 + ty0 + r;
-        if (live[r]) out[(gy - row_begin) * width + gx] = (S)acc[r];
+        const int64_t gy = y0 + ty0 + r;
+        if (gx < width && gy < row_end) out[(gy - row_begin) * width + gx] = (S)acc[r];
     }
+}
+
+template <typename S, typename T, typename WT, int TY>
+int launch_window_ty(const S* z, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
+                     int64_t re, int R, double alpha, const WT* g, S* out, size_t smem,
+                     cudaStream_t s) {
+    constexpr int K3_RB = K3_RB_FOR<TY>::v;
+    auto kern = k_window_sum<S, T, WT, TY, K3_RB>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
+    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - rb + TY - 1) / TY));
+    kern<<<grid, K3_TX * TY / K3_RB, smem, s>>>(z, ld, width, slab_rows, rb, re, R, g, alpha,
+                                                alpha == 2.0 ? 1 : 0, out);
+    return launch_check("polsar_window_distance: launch failed");
+}
+
+constexpr size_t K3_SMEM_MAX = 227 * 1024;
+
+template <typename T, typename WT>
+size_t window_smem(int TY, int R) {
+    return (size_t)(K3_TX + 2 * R) * (TY + 2 * R) * (9 * sizeof(T) + sizeof(WT));
 }
 
 template <typename S, typename T, typename WT>
@@ -620,17 +689,18 @@ int launch_window(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, 
     WT* g = (WT*)ws;
     int64_t n = slab_rows * width;
     k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
-    int HW = K3_TX + 2 * R, HH = K3_TY + 2 * R;
-    size_t smem = (size_t)HW * HH * (9 * sizeof(T) + sizeof(WT));
-    auto kern = k_window_sum<S, T, WT>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
-    double alpha = looks / (2.0 * h);
-    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - rb + K3_TY - 1) / K3_TY));
-    kern<<<grid, K3_THREADS, smem, s>>>(z, ld, width, slab_rows, rb, re, R, g, alpha,
-                                        alpha == 2.0 ? 1 : 0, (S*)outv);
-    return launch_check("polsar_window_distance: launch failed");
+    const double alpha = looks / (2.0 * h);
+    S* out = (S*)outv;
+    if (window_smem<T, WT>(32, R) <= K3_SMEM_MAX)
+        return launch_window_ty<S, T, WT, 32>(z, ld, width, slab_rows, rb, re, R, alpha, g, out,
+                                              window_smem<T, WT>(32, R), s);
+    if (window_smem<T, WT>(16, R) <= K3_SMEM_MAX)
+        return launch_window_ty<S, T, WT, 16>(z, ld, width, slab_rows, rb, re, R, alpha, g, out,
+                                              window_smem<T, WT>(16, R), s);
+    if (window_smem<T, WT>(8, R) <= K3_SMEM_MAX)
+        return launch_window_ty<S, T, WT, 8>(z, ld, width, slab_rows, rb, re, R, alpha, g, out,
+                                             window_smem<T, WT>(8, R), s);
+    return fail(POLSAR_ENOTSUP, "polsar_window_distance: radius too large for shared memory");
 }
 
 // ======================================================= R1: checksums
@@ -707,7 +777,7 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
     if (width < 0 || slab_rows < 0) return fail(POLSAR_EINVAL, "negative size");
     if (out_row_begin < 0 || out_row_end < out_row_begin || out_row_end > slab_rows)
         return fail(POLSAR_EINVAL, "bad output row range");
-    if (radius < 0 || radius > 32) return fail(POLSAR_EINVAL, "radius out of [0, 32]");
+    if (radius < 0 || radius > 16) return fail(POLSAR_EINVAL, "radius out of [0, 16]");
     if (!(looks > 0) || !(h > 0)) return fail(POLSAR_EINVAL, "looks and h must be > 0");
     if (ld < slab_rows * width) return fail(POLSAR_EINVAL, "ld < slab_rows*width");
     if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;

@@ -62,7 +62,7 @@ def test_loads_and_validates_without_gpu():
     assert lib.polsar_inv_det(None, None, None, 0, 0, 0, None) == 0  # n == 0 no-op
     assert lib.polsar_inv_det_cholesky(None, None, None, 4, 4, 9, None) == 1
     assert lib.polsar_window_distance(None, 0, 4, 4, 0, 5, 11, 4.0, 1.0, None, None, 0, None) == 1
-    assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 40, 4.0, 1.0, None, None, 0, None) == 1
+    assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 17, 4.0, 1.0, None, None, 0, None) == 1
     assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 3, 0.0, 1.0, None, None, 0, None) == 1
     assert lib.polsar_checksum(None, 5, 2, 1, 0, 0, None, None, None) == 1
     assert lib.polsar_inv_det_host(None, None, None, 5, 5, 0, 0, None, 0, None, None, None) == 1
