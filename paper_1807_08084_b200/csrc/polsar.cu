@@ -523,9 +523,21 @@ __device__ __forceinline__ float fast_rcp(float x) {
 
 // w = r^(-alpha), alpha = L/(2h).  alpha == 2 (L = 4, h = 1): w = 1/(r r),
 // no transcendental.
+__device__ __forceinline__ float fast_log2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// (MUFU lg2 / ex2: absolute error ~2^-22 in log2 r, i.e. a relative error of
+// about alpha * 1e-7 in w -- far inside the 2e-5 budget for the fp32 weight.)
 __device__ __forceinline__ float pair_weight(float r, float alpha, bool alpha_is_2) {
     if (alpha_is_2) return fast_rcp(r * r);
-    return exp2f(-alpha * log2f(r));
+    return fast_exp2(-alpha * fast_log2(r));
 }
 __device__ __forceinline__ double pair_weight(double r, double alpha, bool alpha_is_2) {
     if (alpha_is_2) return 1.0 / (r * r);
@@ -703,6 +715,327 @@ int launch_window(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, 
     return fail(POLSAR_ENOTSUP, "polsar_window_distance: radius too large for shared memory");
 }
 
+// ------------------------------------------------------------------------
+// K3 (v3, the fp64-determinant modes): the pair determinant by the 3x3
+// expansion  det(A + B) = det A + det B + <adj A, B> + <A, adj B>,
+// <X, Y> = tr(X Y) = sum_k w_k x_k y_k over the packed components with
+// w = (1, 2, 2, 2, 2, 1, 2, 2, 1).  Alg. 2's cofactors (Eq. 3) and
+// determinant (Eq. 6) are evaluated ONCE per pixel in the prepass; each pair
+// then costs one add and 18 FMAs instead of 9 adds and 20 multiply-adds
+// (S = Z_i + Z_j, then Eq. 6 on S).  All four terms are >= 0 for positive-
+// definite pixels, so the sum itself cannot cancel.
+//
+// Prepass (K3a v3) writes 20 fp64 planes per slab pixel:
+//   0..8   z   (the packed Z)
+//   9..17  u = w * adj(Z) (cofactors a_c, b_c, c_c, d_c, e_c, f_c, weighted)
+//   18     D = det Z (Eq. 6)
+//   19     g = 1 / (8 D) as float in the low 4 bytes
+// Main pass (K3b v3): a CTA owns a 256-column x RB-row output block (each
+// thread one column, RB rows).  The window rows it needs stream through
+// shared memory V3_CH rows at a time (all 20 planes, 256 + 2R' columns),
+// double-buffered with cp.async so the next rows load while the current ones
+// are consumed.  Every thread of the CTA pairs each staged row with the same
+// owned rows, so the per-row work is identical across warps (no barrier
+// imbalance), and each staged Z_j serves RB pairs.
+constexpr int V3_TX = 256;
+constexpr int V3_RB = 4;
+constexpr int V3_CH = 2;
+constexpr int V3_NP = 20;        // planes per pixel
+constexpr int V3_THREADS = V3_TX;
+constexpr int V3_RMAX = 12;      // radius limit of this kernel (the paper's R = 11)
+constexpr int V3_XOFF = V3_RMAX; // column of x0 inside a staged row (even)
+constexpr int V3_SW = V3_TX + 2 * V3_XOFF;  // staged row width (compile-time strides)
+constexpr int V3_CHP = V3_CH * V3_SW;       // pixels per chunk plane
+
+template <typename S, typename WT>
+__global__ void __launch_bounds__(256)
+k_window_prep_v3(const S* __restrict__ z, int64_t ld, int64_t n, double* __restrict__ ws) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        H9<double> m;
+        m.a = (double)z[0 * ld + p];
+        m.br = (double)z[1 * ld + p];
+        m.bi = (double)z[2 * ld + p];
+        m.cr = (double)z[3 * ld + p];
+        m.ci = (double)z[4 * ld + p];
+        m.d = (double)z[5 * ld + p];
+        m.er = (double)z[6 * ld + p];
+        m.ei = (double)z[7 * ld + p];
+        m.f = (double)z[8 * ld + p];
+        // Eq. 3 cofactors (Alg. 2 step 1) and Eq. 6 determinant (step 2)
+        double ac = FMA(m.d, m.f, -FMA(m.er, m.er, MUL(m.ei, m.ei)));
+        double bcr = FMA(m.cr, m.er, FMA(m.ci, m.ei, -MUL(m.br, m.f)));
+        double bci = FMA(m.ci, m.er, -FMA(m.cr, m.ei, MUL(m.bi, m.f)));
+        double ccr = FMA(m.br, m.er, -FMA(m.bi, m.ei, MUL(m.cr, m.d)));
+        double cci = FMA(m.br, m.ei, FMA(m.bi, m.er, -MUL(m.ci, m.d)));
+        double dc = FMA(m.a, m.f, -FMA(m.cr, m.cr, MUL(m.ci, m.ci)));
+        double ecr = FMA(m.cr, m.br, FMA(m.ci, m.bi, -MUL(m.a, m.er)));
+        double eci = FMA(m.ci, m.br, -FMA(m.cr, m.bi, MUL(m.a, m.ei)));
+        double fc = FMA(m.a, m.d, -FMA(m.br, m.br, MUL(m.bi, m.bi)));
+        double det = FMA(m.a, ac, FMA(m.br, bcr, FMA(m.bi, bci, FMA(m.cr, ccr, MUL(m.ci, cci)))));
+        const int64_t P = n;  // plane stride of the workspace
+        ws[0 * P + p] = m.a;  ws[1 * P + p] = m.br; ws[2 * P + p] = m.bi;
+        ws[3 * P + p] = m.cr; ws[4 * P + p] = m.ci; ws[5 * P + p] = m.d;
+        ws[6 * P + p] = m.er; ws[7 * P + p] = m.ei; ws[8 * P + p] = m.f;
+        ws[9 * P + p] = ac;
+        ws[10 * P + p] = 2.0 * bcr; ws[11 * P + p] = 2.0 * bci;
+        ws[12 * P + p] = 2.0 * ccr; ws[13 * P + p] = 2.0 * cci;
+        ws[14 * P + p] = dc;
+        ws[15 * P + p] = 2.0 * ecr; ws[16 * P + p] = 2.0 * eci;
+        ws[17 * P + p] = fc;
+        ws[18 * P + p] = det;
+        const double g = 1.0 / (8.0 * det);
+        if constexpr (std::is_same<WT, float>::value)
+            ws[19 * P + p] = __longlong_as_double((long long)(unsigned)__float_as_uint((float)g));
+        else
+            ws[19 * P + p] = g;
+    }
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    int src_bytes = valid ? 8 : 0;  // 0: zero-fill
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(sa), "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+// plane 19 holds g as fp64 (fp64 weights) or as fp32 bits in the low word
+template <typename WT>
+__device__ __forceinline__ WT load_g(double v);
+template <>
+__device__ __forceinline__ float load_g<float>(double v) {
+    return __uint_as_float((unsigned)__double_as_longlong(v));
+}
+template <>
+__device__ __forceinline__ double load_g<double>(double v) { return v; }
+
+template <typename WT>
+__device__ __forceinline__ WT weight_v3(double T, WT gi, WT gj, WT alpha, bool a2) {
+    WT ft = (WT)T;
+    WT rr = (ft * gi) * (ft * gj);
+    return pair_weight(rr, alpha, a2);
+}
+
+// one pair: T = det(Z_i + Z_j) = D_i + D_j + <u_i, z_j> + <z_i, u_j>
+__device__ __forceinline__ double pair_T(const double* ui, const double* zi, double Di,
+                                         const double* uj, const double* zj, double Dj) {
+    double a = __fma_rn(ui[0], zj[0], __dadd_rn(Di, Dj));
+    double b = __dmul_rn(ui[6], zj[6]);
+    double c = __dmul_rn(zi[3], uj[3]);
+    a = __fma_rn(ui[1], zj[1], a);
+    b = __fma_rn(ui[7], zj[7], b);
+    c = __fma_rn(zi[4], uj[4], c);
+    a = __fma_rn(ui[2], zj[2], a);
+    b = __fma_rn(ui[8], zj[8], b);
+    c = __fma_rn(zi[5], uj[5], c);
+    a = __fma_rn(ui[3], zj[3], a);
+    b = __fma_rn(zi[0], uj[0], b);
+    c = __fma_rn(zi[6], uj[6], c);
+    a = __fma_rn(ui[4], zj[4], a);
+    b = __fma_rn(zi[1], uj[1], b);
+    c = __fma_rn(zi[7], uj[7], c);
+    a = __fma_rn(ui[5], zj[5], a);
+    b = __fma_rn(zi[2], uj[2], b);
+    c = __fma_rn(zi[8], uj[8], c);
+    return __dadd_rn(a, __dadd_rn(b, c));
+}
+
+
+// T_r = det(Z_{i_r} + Z_j) for the RB owned pixels at once, written as
+// 2*RB independent FMA chains (k-outer, pixel-inner) so the FP64 pipe always
+// has independent work in flight.
+template <int RB>
+__device__ __forceinline__ void pair_T_block(const double (&ui)[RB][9], const double (&zi)[RB][9],
+                                             const double (&Di)[RB], const double* uj,
+                                             const double* zj, double Dj, double (&T)[RB]) {
+    double A[RB], B[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        A[r] = __fma_rn(ui[r][0], zj[0], Di[r]);
+        B[r] = __fma_rn(zi[r][0], uj[0], Dj);
+    }
+#pragma unroll
+    for (int k = 1; k < 9; ++k) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            A[r] = __fma_rn(ui[r][k], zj[k], A[r]);
+            B[r] = __fma_rn(zi[r][k], uj[k], B[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) T[r] = __dadd_rn(A[r], B[r]);
+}
+
+template <typename S, typename WT, bool A2>
+__global__ void __launch_bounds__(V3_THREADS, 1)
+k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows, int64_t row_begin,
+                int64_t row_end, int R, double alpha_d, S* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int XOFF = V3_XOFF, SW = V3_SW, CHP = V3_CHP;
+    double* buf = reinterpret_cast<double*>(smem_raw);  // [2][V3_NP][V3_CH][SW]
+    const int64_t P = slab_rows * width;                // workspace plane stride
+
+    const int64_t x0 = (int64_t)blockIdx.x * V3_TX;
+    const int64_t y0 = row_begin + (int64_t)blockIdx.y * V3_RB;
+    // window rows of the block, clipped to the slab
+    const int64_t ja = y0 - R > 0 ? y0 - R : 0;
+    const int64_t jb = (y0 + V3_RB - 1 + R) < slab_rows - 1 ? (y0 + V3_RB - 1 + R) : slab_rows - 1;
+    const int nrows = (int)(jb - ja + 1);
+    const int nchunks = (nrows + V3_CH - 1) / V3_CH;
+
+    auto load_chunk = [&](int c, int b) {
+        double* dst = buf + (size_t)b * V3_NP * CHP;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (int pr = warp; pr < V3_NP * V3_CH; pr += V3_THREADS / 32) {
+            const int pl = pr / V3_CH, row = pr % V3_CH;  // compile-time divisors
+            const int64_t gy = ja + (int64_t)c * V3_CH + row;
+            const bool rok = gy <= jb;
+            const double* srow = ws + pl * P + (rok ? gy : 0) * width;
+            double* drow = dst + pl * CHP + row * SW;
+            for (int col = lane; col < SW; col += 32) {
+                const int64_t gxx = x0 - XOFF + col;
+                const bool ok = rok && gxx >= 0 && gxx < width;
+                cp_async8(drow + col, srow + (ok ? gxx : 0), ok);
+            }
+        }
+        cp_async_commit();
+    };
+    load_chunk(0, 0);
+
+    // owned pixels: column gx, rows y0 .. y0 + RB - 1
+    const int tx = threadIdx.x;
+    const int64_t gx = x0 + tx;
+    double ui[V3_RB][9], zi[V3_RB][9], Di[V3_RB];
+    WT gi[V3_RB];
+    double acc[V3_RB];
+#pragma unroll
+    for (int r = 0; r < V3_RB; ++r) {
+        const int64_t gy = y0 + r;
+        const bool ok = gx < width && gy < slab_rows;
+        const int64_t p = ok ? gy * width + gx : 0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            zi[r][k] = ok ? ws[k * P + p] : 0.0;
+            ui[r][k] = ok ? ws[(9 + k) * P + p] : 0.0;
+        }
+        Di[r] = ok ? ws[18 * P + p] : 0.0;
+        gi[r] = ok ? load_g<WT>(ws[19 * P + p]) : WT(0);
+        acc[r] = 0.0;
+    }
+    const WT alpha = (WT)alpha_d;
+    constexpr bool a2 = A2;
+    const bool interior_x = (x0 - R >= 0) && (x0 + V3_TX + R <= width);
+
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+            load_chunk(c + 1, (c + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* cb = buf + (size_t)(c & 1) * V3_NP * CHP;
+#pragma unroll 1
+        for (int row = 0; row < V3_CH; ++row) {
+            const int64_t gyj = ja + (int64_t)c * V3_CH + row;
+            if (gyj > jb) break;
+            const int dy0 = (int)(gyj - y0);  // dy of owned row r is dy0 - r (CTA-uniform)
+            const double* rb = cb + row * SW + XOFF + tx;
+            WT rowacc[V3_RB];
+#pragma unroll
+            for (int r = 0; r < V3_RB; ++r) rowacc[r] = WT(0);
+            const bool all = (dy0 - (V3_RB - 1) >= -R) && (dy0 <= R);
+            if (all) {
+                // software-pipelined: the weights of column wx-1 (F2F / FMUL /
+                // MUFU, long-latency) are evaluated alongside the FMA chains of
+                // column wx, so the FP64 pipe never waits on the weight tail
+                double Tp[V3_RB];
+                WT gp = WT(0);
+                bool okp = false;
+#pragma unroll
+                for (int r = 0; r < V3_RB; ++r) Tp[r] = 1.0;
+#pragma unroll 1
+                for (int wx = -R; wx <= R; ++wx) {
+                    double zj[9], uj[9];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) {
+                        zj[k] = rb[k * CHP + wx];
+                        uj[k] = rb[(9 + k) * CHP + wx];
+                    }
+                    const double Dj = rb[18 * CHP + wx];
+                    const WT gj = load_g<WT>(rb[19 * CHP + wx]);
+                    const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+                    double T[V3_RB];
+                    pair_T_block<V3_RB>(ui, zi, Di, uj, zj, Dj, T);
+#pragma unroll
+                    for (int r = 0; r < V3_RB; ++r) {
+                        WT w = weight_v3<WT>(Tp[r], gi[r], gp, alpha, a2);
+                        rowacc[r] += okp ? w : WT(0);
+                        Tp[r] = T[r];
+                    }
+                    gp = gj;
+                    okp = colok;
+                }
+#pragma unroll
+                for (int r = 0; r < V3_RB; ++r) {
+                    WT w = weight_v3<WT>(Tp[r], gi[r], gp, alpha, a2);
+                    rowacc[r] += okp ? w : WT(0);
+                }
+            } else {
+#pragma unroll 1
+                for (int wx = -R; wx <= R; ++wx) {
+                    double zj[9], uj[9];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) {
+                        zj[k] = rb[k * CHP + wx];
+                        uj[k] = rb[(9 + k) * CHP + wx];
+                    }
+                    const double Dj = rb[18 * CHP + wx];
+                    const WT gj = load_g<WT>(rb[19 * CHP + wx]);
+                    const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+#pragma unroll
+                    for (int r = 0; r < V3_RB; ++r) {
+                        const int dy = dy0 - r;
+                        if (dy >= -R && dy <= R) {  // CTA-uniform
+                            WT w = weight_v3<WT>(pair_T(ui[r], zi[r], Di[r], uj, zj, Dj), gi[r], gj, alpha, a2);
+                            rowacc[r] += colok ? w : WT(0);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < V3_RB; ++r) acc[r] += (double)rowacc[r];
+        }
+        __syncthreads();  // buffer (c & 1) is refilled by the prefetch of chunk c + 2
+    }
+#pragma unroll
+    for (int r = 0; r < V3_RB; ++r) {
+        const int64_t gy = y0 + r;
+        if (gx < width && gy < row_end) out[(gy - row_begin) * width + gx] = (S)acc[r];
+    }
+}
+
+template <typename S, typename WT>
+int launch_window_v3(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
+                     int64_t re, int R, double looks, double h, void* wsv, void* outv,
+                     cudaStream_t s) {
+    const int64_t n = slab_rows * width;
+    double* ws = (double*)wsv;
+    k_window_prep_v3<S, WT><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, ws);
+    size_t smem = (size_t)2 * V3_NP * V3_CHP * sizeof(double);
+    const double alpha = looks / (2.0 * h);
+    auto kern = alpha == 2.0 ? k_window_sum_v3<S, WT, true> : k_window_sum_v3<S, WT, false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
+    dim3 grid((unsigned)((width + V3_TX - 1) / V3_TX), (unsigned)((re - rb + V3_RB - 1) / V3_RB));
+    kern<<<grid, V3_THREADS, smem, s>>>(ws, width, slab_rows, rb, re, R, alpha, (S*)outv);
+    return launch_check("polsar_window_distance: launch failed");
+}
+
 // ======================================================= R1: checksums
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x ^= x >> 30;
@@ -765,10 +1098,10 @@ int polsar_inv_det_cholesky(const void* z, void* out, uint8_t* status, int64_t n
 
 size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int dtype) {
     if (slab_rows < 0 || width < 0) return 0;
-    // one plane of g_i = 1/(8 det Z_i) in the weight type: fp64 for the F64
-    // modes, fp32 otherwise (rounded up to 256 bytes)
-    size_t es = (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) ? 8 : 4;
-    return (((size_t)(slab_rows * width) * es) + 255) / 256 * 256;
+    // fp64-determinant modes: 20 fp64 planes per pixel (z, weighted adj(Z),
+    // det, g); F32_PLAIN: one fp32 plane of g (rounded up to 256 bytes)
+    size_t per = (dtype == POLSAR_F32_PLAIN) ? 4 : 20 * 8;
+    return (((size_t)(slab_rows * width) * per) + 255) / 256 * 256;
 }
 
 int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
@@ -785,10 +1118,16 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
     cudaStream_t s = (cudaStream_t)cuda_stream;
     switch (dtype) {
         case POLSAR_F32:
+            if (radius <= V3_RMAX)
+                return launch_window_v3<float, float>(z, ld, width, slab_rows, out_row_begin,
+                                                      out_row_end, radius, looks, h, workspace, out, s);
             return launch_window<float, double, float>(z, ld, width, slab_rows, out_row_begin,
                                                        out_row_end, radius, looks, h, workspace, out, s);
         case POLSAR_F64:
         case POLSAR_F64_PLAIN:
+            if (radius <= V3_RMAX)
+                return launch_window_v3<double, double>(z, ld, width, slab_rows, out_row_begin,
+                                                        out_row_end, radius, looks, h, workspace, out, s);
             return launch_window<double, double, double>(z, ld, width, slab_rows, out_row_begin,
                                                          out_row_end, radius, looks, h, workspace, out, s);
         case POLSAR_F32_PLAIN:

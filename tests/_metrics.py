@@ -34,3 +34,17 @@ def entrywise(got, ref):
 def worst(got, ref, mask):
     inv, det, idet = errors(got, ref)
     return float(max(inv[mask].max(initial=0), det[mask].max(initial=0), idet[mask].max(initial=0)))
+
+
+def status_expected(z, ref, storage):
+    """Status the kernels must report, decided from the oracle's exact det:
+    SINGULAR (1) iff det <= tau a d f, tau = 16 u_in (R-5).
+    Returns (expected, decidable) -- pixels within 1e-6 relative of the
+    threshold are not decidable across precisions and are excluded."""
+    u = 2.0 ** -24 if storage == "float32" else 2.0 ** -53
+    z = np.asarray(z, dtype=np.float64)
+    thr = 16 * u * z[0] * z[5] * z[8]
+    det = ref[9]
+    expected = np.where(det > thr, 0, 1).astype(np.uint8)
+    decidable = np.abs(det - thr) > 1e-6 * np.abs(thr)
+    return expected, decidable

@@ -12,7 +12,10 @@ from paper_1807_08084_b200 import configs, wishart
 
 pytestmark = pytest.mark.gpu
 THREADS = len(os.sched_getaffinity(0))
-TOL = {torch.float32: 2e-5, torch.float64: 1e-12}
+# fp32 storage: BASELINE's 2e-5.  fp64 storage (not a BASELINE config): the
+# pair determinant carries a relative error <= ~81 kappa u (expansion form,
+# DESIGN.md K3) and the weight multiplies it by 2 alpha = 4: 4*81*1e4*2^-53 ~ 4e-10.
+TOL = {torch.float32: 2e-5, torch.float64: 4e-10}
 
 
 def clipped_counts(h, w, r):
@@ -23,7 +26,8 @@ def clipped_counts(h, w, r):
 
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
-@pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 53), 3), ((20, 70), 0), ((150, 33), 11)])
+@pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 53), 3), ((20, 70), 0), ((150, 33), 11),
+                                          ((300, 270), 11), ((40, 45), 14)])
 def test_window_parity(cuda, dt, shape, radius):
     h, w = shape
     cfg = configs.get("c5").scaled(h, w)
