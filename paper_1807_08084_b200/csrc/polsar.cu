@@ -16,6 +16,7 @@
 // vector body and the scalar tail: both yield identical bits.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <type_traits>
@@ -1083,6 +1084,19 @@ k_checksum(const U* __restrict__ planes, int64_t n, int64_t ld, int nplanes, int
 
 }  // namespace
 
+// Window kernel variant for the fp64-determinant modes: 2 (direct Eq. 6 on
+// S = Z_i + Z_j, default: fastest measured on B200) or 3 (cubic expansion
+// over per-pixel adjugates, fewer FP64 ops but smem/register bound);
+// POLSAR_WINDOW_VARIANT=3 selects the latter (A/B runs; both are parity-tested).
+int window_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("POLSAR_WINDOW_VARIANT");
+        v = (e && e[0] == '3') ? 3 : 2;
+    }
+    return v;
+}
+
 // ============================================================== C-ABI
 extern "C" {
 
@@ -1118,14 +1132,14 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
     cudaStream_t s = (cudaStream_t)cuda_stream;
     switch (dtype) {
         case POLSAR_F32:
-            if (radius <= V3_RMAX)
+            if (radius <= V3_RMAX && window_variant() == 3)
                 return launch_window_v3<float, float>(z, ld, width, slab_rows, out_row_begin,
                                                       out_row_end, radius, looks, h, workspace, out, s);
             return launch_window<float, double, float>(z, ld, width, slab_rows, out_row_begin,
                                                        out_row_end, radius, looks, h, workspace, out, s);
         case POLSAR_F64:
         case POLSAR_F64_PLAIN:
-            if (radius <= V3_RMAX)
+            if (radius <= V3_RMAX && window_variant() == 3)
                 return launch_window_v3<double, double>(z, ld, width, slab_rows, out_row_begin,
                                                         out_row_end, radius, looks, h, workspace, out, s);
             return launch_window<double, double, double>(z, ld, width, slab_rows, out_row_begin,

@@ -46,9 +46,10 @@ def check_sampled(cfg, tab, z, out, status, idx, tol):
     return k, inv, det
 
 
-def full_properties(out, status, dt):
+def full_properties(out, status, dt, algo="adjugate"):
     """Every pixel: OK pixels are finite with det > 0 and det * t within
-    rounding of 1."""
+    rounding of 1 (Alg. 2: t = RN(1/det), a few u; Alg. 1: det and det^-1
+    are separate products of rounded factors (R-14), ~6 roundings each)."""
     ok = status == 0
     n_ok = int(ok.sum())
     assert n_ok > 0.98 * status.numel()
@@ -58,7 +59,7 @@ def full_properties(out, status, dt):
     t = out[10][ok].double()
     assert bool((det > 0).all())
     u = 2.0 ** -24 if dt == torch.float32 else 2.0 ** -53
-    assert float((det * t - 1).abs().max()) <= 4 * u
+    assert float((det * t - 1).abs().max()) <= (4 if algo == "adjugate" else 16) * u
 
 
 @pytest.fixture(scope="module")
@@ -82,7 +83,7 @@ def test_c3_full_size(c3, algo):
     torch.cuda.synchronize()
     idx = sample_pixels(n, cfg.width, seed=3)
     check_sampled(cfg, tab, z, out, status, idx, TOL["float32"])
-    full_properties(out, status, torch.float32)
+    full_properties(out, status, torch.float32, algo)
     del out, status
 
 
@@ -105,6 +106,6 @@ def test_c4_full_size(cuda, algo):
     assert near.sum() > 100
     print(f"\n[report] c4 near-singular pixels: {int(near.sum())} sampled, "
           f"max normwise inverse error {inv[near].max():.2e}, det {det[near].max():.2e}")
-    full_properties(out, status, torch.float64)
+    full_properties(out, status, torch.float64, algo)
     del out, status, z
     torch.cuda.empty_cache()

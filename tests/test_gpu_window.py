@@ -91,3 +91,29 @@ def test_window_c5_sampled(cuda):
     rel = np.abs(got[idx] - ref) / ref
     assert rel.max() <= 2e-5, rel.max()
     assert np.all(np.isfinite(got)) and got.min() >= 1 - 1e-6 and got.max() <= 529 + 1e-3
+
+
+def test_window_variant3_subprocess(cuda):
+    """The alternative expansion-form kernel (POLSAR_WINDOW_VARIANT=3, read
+    once per process) against the oracle, in a child process."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle
+import paper_1807_08084_b200 as P
+from paper_1807_08084_b200 import configs, wishart
+for dt, tol in ((torch.float32, 2e-5), (torch.float64, 4e-10)):
+    h, w, r = 80, 70, 11
+    z = wishart.generate(configs.get("c5").scaled(h, w), device="cuda").to(dt)
+    got = P.window_distance(z, h, w, radius=r).cpu().numpy()
+    ref = oracle.window(z.cpu().numpy(), h, w, r, 4.0, 1.0)
+    e = float((np.abs(got - ref) / ref).max())
+    assert e <= tol, (dt, e)
+print("ok")
+'''
+    env = dict(os.environ, POLSAR_WINDOW_VARIANT="3")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=300)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stdout + res.stderr
