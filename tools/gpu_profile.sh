@@ -19,7 +19,7 @@ $PROF > $OUT/prof_plain.json 2> $OUT/prof_plain.err && \
   $NCU --set full --clock-control none --import-source on --kernel-name-base mangled \
        -k regex:k_inv_det_vecIfLi1ELi0E -s 2 -c 1 -o $OUT/prof_k2 -f $PROF > $OUT/ncu_k2.log 2>&1 && \
   $NCU --set full --clock-control none --import-source on --kernel-name-base mangled \
-       -k regex:k_window_sumIfdf -s 1 -c 1 -o $OUT/prof_k3 -f $PROF > $OUT/ncu_k3.log 2>&1 && \
+       -k regex:k_window_sumIfdfLi32 -s 1 -c 1 -o $OUT/prof_k3 -f $PROF > $OUT/ncu_k3.log 2>&1 && \
   $NCU --set full --clock-control none --import-source on --kernel-name-base mangled \
-       -k regex:k_window_sumIfff -s 1 -c 1 -o $OUT/prof_k3_plain -f $PROF > $OUT/ncu_k3p.log 2>&1
+       -k regex:k_window_sumIfffLi32 -s 1 -c 1 -o $OUT/prof_k3_plain -f $PROF > $OUT/ncu_k3p.log 2>&1
 echo "ncu full rc=$?"
