@@ -92,6 +92,19 @@ int polsar_inv_det(const void* z, void* out, uint8_t* status, int64_t n, int64_t
 int polsar_inv_det_cholesky(const void* z, void* out, uint8_t* status, int64_t n, int64_t ld,
                             int dtype, void* cuda_stream);
 
+/* polsar_inv_det_blocks -- multi-frequency PolSAR pixels whose covariance is
+ * block diagonal with nblocks Hermitian 3x3 blocks, one per frequency band
+ * (PAPER.md:1043-1055 [§V]): Alg. 2 on each block.
+ *   z      : device, 9*nblocks planes (block b at planes 9b..9b+8, field order
+ *            as above), plane stride ld
+ *   out    : device, 9*nblocks + 2 planes: block inverses at 9b..9b+8, then
+ *            det and det^-1 of the whole block-diagonal matrix (products of
+ *            the block values in the arithmetic type, rounded once)
+ *   status : device, n bytes or NULL: the worst block status
+ *   nblocks: 1..64;  dtype, ownership and errors as polsar_inv_det. */
+int polsar_inv_det_blocks(const void* z, void* out, uint8_t* status, int64_t n, int64_t ld,
+                          int nblocks, int dtype, void* cuda_stream);
+
 /* polsar_window_workspace_bytes -- bytes of device workspace
  * polsar_window_distance needs for a slab of slab_rows x width pixels. */
 size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int dtype);

@@ -57,6 +57,8 @@ def lib() -> ctypes.CDLL:
         _lib.oracle_pair_distance.restype = D
         _lib.oracle_window_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
         _lib.oracle_window_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+        _lib.oracle_inv_det_blocks_f64.argtypes = [P, I64, INT, P, I64, I64]
+        _lib.oracle_inv_det_blocks_f32.argtypes = [P, I64, INT, P, I64, I64]
         _lib.oracle_ldbl_mant_dig.restype = INT
         _lib.oracle_quad_mant_dig.restype = INT
     return _lib
@@ -89,6 +91,21 @@ def inv_det(z: np.ndarray, with_imag: bool = False):
     fn = lib().oracle_inv_det_f64 if z.dtype == np.float64 else lib().oracle_inv_det_f32
     fn(_ptr(z), n, _ptr(out), n, _ptr(im) if im is not None else None, n)
     return (out, im) if with_imag else out
+
+
+def inv_det_blocks(z: np.ndarray, nblocks: int) -> np.ndarray:
+    """Multi-frequency block-diagonal pixels: z has
+    9*nblocks planes; returns (9*nblocks + 2, n) -- block inverses, det and
+    det^-1 of the whole block-diagonal matrix (binary128, blockwise cofactor
+    definition, products of the block determinants)."""
+    z = np.ascontiguousarray(np.asarray(z))
+    if z.ndim != 2 or z.shape[0] != 9 * nblocks:
+        raise ValueError("z must have shape (9*nblocks, n)")
+    n = z.shape[1]
+    out = np.empty((9 * nblocks + 2, n), dtype=np.float64)
+    fn = lib().oracle_inv_det_blocks_f64 if z.dtype == np.float64 else lib().oracle_inv_det_blocks_f32
+    fn(_ptr(z), n, int(nblocks), _ptr(out), n, n)
+    return out
 
 
 def inv_det_threaded(z: np.ndarray, threads: int) -> np.ndarray:

@@ -153,6 +153,59 @@ void oracle_inv_det_f32(const float* z, int64_t ldz, double* out, int64_t ldo,
     }
 }
 
+/* Multi-frequency block-diagonal matrices (PAPER.md:1043-1055 [§V]): a pixel
+ * holds nblocks Hermitian 3x3 diagonal blocks; its inverse is the block
+ * diagonal of the block inverses and its determinant the product of the block
+ * determinants ("obtained after applications of the proposed method to each of
+ * the diagonal blocks").  z: 9*nblocks planes (block b at planes 9b..9b+8);
+ * out: 9*nblocks + 2 planes (block inverses, then det and det^-1 of the whole
+ * matrix).  Block values by the cofactor definition above, in binary128. */
+void oracle_inv_det_blocks_f64(const double* z, int64_t ldz, int nblocks, double* out,
+                               int64_t ldo, int64_t n) {
+    for (int64_t p = 0; p < n; ++p) {
+        q_t det_all = 1, inv_all = 1;
+        for (int b = 0; b < nblocks; ++b) {
+            herm_q m = load_q_f64(z + (int64_t)9 * b * ldz, ldz, p);
+            herm_q c = cofactors_q(m);
+            q_t re, im;
+            det_full_q(m, c, &re, &im);
+            double* o = out + (int64_t)9 * b * ldo;
+            o[0 * ldo + p] = (double)(c.a / re);  o[1 * ldo + p] = (double)(c.br / re);
+            o[2 * ldo + p] = (double)(c.bi / re); o[3 * ldo + p] = (double)(c.cr / re);
+            o[4 * ldo + p] = (double)(c.ci / re); o[5 * ldo + p] = (double)(c.d / re);
+            o[6 * ldo + p] = (double)(c.er / re); o[7 * ldo + p] = (double)(c.ei / re);
+            o[8 * ldo + p] = (double)(c.f / re);
+            det_all *= re;
+            inv_all /= re;
+        }
+        out[((int64_t)9 * nblocks) * ldo + p] = (double)det_all;
+        out[((int64_t)9 * nblocks + 1) * ldo + p] = (double)inv_all;
+    }
+}
+
+void oracle_inv_det_blocks_f32(const float* z, int64_t ldz, int nblocks, double* out,
+                               int64_t ldo, int64_t n) {
+    for (int64_t p = 0; p < n; ++p) {
+        q_t det_all = 1, inv_all = 1;
+        for (int b = 0; b < nblocks; ++b) {
+            herm_q m = load_q_f32(z + (int64_t)9 * b * ldz, ldz, p);
+            herm_q c = cofactors_q(m);
+            q_t re, im;
+            det_full_q(m, c, &re, &im);
+            double* o = out + (int64_t)9 * b * ldo;
+            o[0 * ldo + p] = (double)(c.a / re);  o[1 * ldo + p] = (double)(c.br / re);
+            o[2 * ldo + p] = (double)(c.bi / re); o[3 * ldo + p] = (double)(c.cr / re);
+            o[4 * ldo + p] = (double)(c.ci / re); o[5 * ldo + p] = (double)(c.d / re);
+            o[6 * ldo + p] = (double)(c.er / re); o[7 * ldo + p] = (double)(c.ei / re);
+            o[8 * ldo + p] = (double)(c.f / re);
+            det_all *= re;
+            inv_all /= re;
+        }
+        out[((int64_t)9 * nblocks) * ldo + p] = (double)det_all;
+        out[((int64_t)9 * nblocks + 1) * ldo + p] = (double)inv_all;
+    }
+}
+
 /* ---------------------------------------------------------------------------
  * Brute force: complex Gauss-Jordan elimination with partial pivoting on the
  * full 3x3 matrix (no cofactors involved).  Independent check of the

@@ -22,7 +22,7 @@ POLSAR_F32, POLSAR_F64, POLSAR_F32_PLAIN, POLSAR_F64_PLAIN = 0, 1, 2, 3
 STATUS_OK, STATUS_SINGULAR, STATUS_NOT_PD = 0, 1, 2
 
 __all__ = [
-    "polsar_inv_det", "polsar_inv_det_cholesky", "polsar_window_distance",
+    "polsar_inv_det", "polsar_inv_det_cholesky", "polsar_inv_det_blocks", "polsar_window_distance",
     "polsar_window_workspace_bytes", "polsar_checksum", "polsar_inv_det_host",
     "polsar_host_chunk_pixels", "inv_det", "window_distance", "dtype_code", "PolsarError",
     "POLSAR_F32", "POLSAR_F64", "POLSAR_F32_PLAIN", "POLSAR_F64_PLAIN",
@@ -93,6 +93,24 @@ def polsar_inv_det(z, out, status=None, n=None, plain=False, stream=None):
 def polsar_inv_det_cholesky(z, out, status=None, n=None, plain=False, stream=None):
     """Alg. 1 (PAPER.md:279-378, l21 corrected) on every pixel."""
     return _inv_det_call("polsar_inv_det_cholesky", z, out, status, n, plain, stream)
+
+
+def polsar_inv_det_blocks(z, out, nblocks, status=None, n=None, plain=False, stream=None):
+    """Multi-frequency block-diagonal pixels: z is
+    (9*nblocks, ld), out (9*nblocks + 2, ld)."""
+    _dev_check(z, out, status)
+    ldz = _planes(z, 9 * nblocks)
+    if _planes(out, 9 * nblocks + 2) != ldz:
+        raise ValueError("z and out must share the plane stride ld")
+    if out.dtype != z.dtype:
+        raise TypeError("z and out must have the same dtype")
+    n = z.shape[1] if n is None else int(n)
+    if status is not None and (status.dtype != _torch().uint8 or status.numel() < n):
+        raise ValueError("status must be a uint8 tensor of >= n elements")
+    rc = lib().polsar_inv_det_blocks(_ptr(z), _ptr(out), _ptr(status), n, ldz, int(nblocks),
+                                     dtype_code(z.dtype, plain), _stream_ptr(stream))
+    check(rc, "polsar_inv_det_blocks")
+    return out
 
 
 def inv_det(z, algo: str = "adjugate", plain: bool = False, with_status: bool = True,

@@ -22,6 +22,7 @@ U64P = ctypes.c_void_p
 SIGNATURES = {
     "polsar_inv_det": (INT, [P, P, U8P, I64, I64, INT, P]),
     "polsar_inv_det_cholesky": (INT, [P, P, U8P, I64, I64, INT, P]),
+    "polsar_inv_det_blocks": (INT, [P, P, U8P, I64, I64, INT, INT, P]),
     "polsar_window_workspace_bytes": (SZ, [I64, I64, INT]),
     "polsar_window_distance": (INT, [P, I64, I64, I64, I64, I64, INT, D, D, P, P, INT, P]),
     "polsar_checksum": (INT, [P, I64, I64, INT, INT, I64, U8P, U64P, P]),

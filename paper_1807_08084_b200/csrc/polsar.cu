@@ -265,9 +265,17 @@ __device__ __forceinline__ bool alg1(const H9<T>& m, T* o, T& det, T& tdet) {
 enum { ALGO_ADJ = 0, ALGO_CHOL = 1 };
 enum { MATH_F64 = 0, MATH_F64_EFT = 1, MATH_F32 = 2 };
 
+template <int MATH>
+struct MathT {
+    typedef typename std::conditional<MATH == MATH_F32, float, double>::type type;
+};
+
+// One matrix: inverse (9 values in the arithmetic type), det, t, status.
 template <typename S, int ALGO, int MATH>
-__device__ __forceinline__ void solve_one(const S* in, S* out, uint8_t& st) {
-    typedef typename std::conditional<MATH == MATH_F32, float, double>::type T;
+__device__ __forceinline__ uint8_t solve_core(const S* in, typename MathT<MATH>::type* o,
+                                              typename MathT<MATH>::type& det,
+                                              typename MathT<MATH>::type& t) {
+    typedef typename MathT<MATH>::type T;
     H9<T> m;
     m.a = (T)in[0];
     m.br = (T)in[1];
@@ -278,7 +286,6 @@ __device__ __forceinline__ void solve_one(const S* in, S* out, uint8_t& st) {
     m.er = (T)in[6];
     m.ei = (T)in[7];
     m.f = (T)in[8];
-    T o[9], det, t;
     bool pd = true;
     if constexpr (ALGO == ALGO_ADJ) {
         if constexpr (MATH == MATH_F64_EFT)
@@ -288,15 +295,22 @@ __device__ __forceinline__ void solve_one(const S* in, S* out, uint8_t& st) {
     } else {
         pd = alg1<T>(m, o, det, t);
     }
+    // full-rank check (PAPER.md:469-476) as a scaled threshold (R-5)
+    T thr = MUL(MUL(MUL((T)Tau<S>::v, m.a), m.d), m.f);
+    bool ok = (det > thr) && finite_pos(det) && finite_pos(t);
+    return !pd ? (uint8_t)POLSAR_STATUS_NOT_PD
+               : (ok ? (uint8_t)POLSAR_STATUS_OK : (uint8_t)POLSAR_STATUS_SINGULAR);
+}
+
+template <typename S, int ALGO, int MATH>
+__device__ __forceinline__ void solve_one(const S* in, S* out, uint8_t& st) {
+    typedef typename MathT<MATH>::type T;
+    T o[9], det, t;
+    st = solve_core<S, ALGO, MATH>(in, o, det, t);
 #pragma unroll
     for (int k = 0; k < 9; ++k) out[k] = (S)o[k];
     out[9] = (S)det;
     out[10] = (S)t;
-    // full-rank check (PAPER.md:469-476) as a scaled threshold (R-5)
-    T thr = MUL(MUL(MUL((T)Tau<S>::v, m.a), m.d), m.f);
-    bool ok = (det > thr) && finite_pos(det) && finite_pos(t);
-    st = !pd ? (uint8_t)POLSAR_STATUS_NOT_PD : (ok ? (uint8_t)POLSAR_STATUS_OK
-                                                   : (uint8_t)POLSAR_STATUS_SINGULAR);
 }
 
 // --------------------------------------------------------------- K1 / K2
@@ -438,6 +452,116 @@ int launch_inv_det(const void* zv, void* outv, uint8_t* status, int64_t n, int64
     }
     return launch_check(ALGO == ALGO_ADJ ? "polsar_inv_det: launch failed"
                                          : "polsar_inv_det_cholesky: launch failed");
+}
+
+// ------------------------------------------------ multi-frequency blocks
+// PAPER.md:1043-1055 [§V]: a pixel holds nblocks Hermitian 3x3 diagonal
+// blocks (one per frequency band).  Alg. 2 runs on each block; the whole
+// matrix's det and det^-1 are the products of the blocks' (in the arithmetic
+// type, rounded once); status is the worst block status.  Planes: input block
+// b at 9b..9b+8; output block inverses at 9b..9b+8, det at 9B, det^-1 at 9B+1.
+template <typename S, int MATH>
+__global__ void __launch_bounds__(K1_THREADS)
+k_inv_det_blocks_vec(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
+                     int64_t n_groups, int64_t ld, int nblocks) {
+    typedef typename Vec<S>::type V;
+    typedef typename MathT<MATH>::type T;
+    constexpr int W = Vec<S>::n;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_groups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = g * W;
+        T det_all[W], t_all[W];
+        uint8_t st[W];
+#pragma unroll
+        for (int v = 0; v < W; ++v) {
+            det_all[v] = T(1);
+            t_all[v] = T(1);
+            st[v] = 0;
+        }
+        for (int b = 0; b < nblocks; ++b) {
+            const S* zb = z + (int64_t)9 * b * ld;
+            S* ob = out + (int64_t)9 * b * ld;
+            S in[9][W];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) unpack<V, S>(ld_stream(reinterpret_cast<const V*>(zb + k * ld + p)), in[k]);
+            S res[9][W];
+#pragma unroll
+            for (int v = 0; v < W; ++v) {
+                S x[9];
+                T o[9], det, t;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) x[k] = in[k][v];
+                uint8_t s1 = solve_core<S, ALGO_ADJ, MATH>(x, o, det, t);
+                st[v] = s1 > st[v] ? s1 : st[v];
+                det_all[v] = MUL(det_all[v], det);
+                t_all[v] = MUL(t_all[v], t);
+#pragma unroll
+                for (int k = 0; k < 9; ++k) res[k][v] = (S)o[k];
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                st_stream(reinterpret_cast<V*>(ob + k * ld + p), packv(res[k], (V*)nullptr));
+        }
+        S dd[W], tt[W];
+#pragma unroll
+        for (int v = 0; v < W; ++v) {
+            dd[v] = (S)det_all[v];
+            tt[v] = (S)t_all[v];
+        }
+        S* oe = out + (int64_t)9 * nblocks * ld;
+        st_stream(reinterpret_cast<V*>(oe + p), packv(dd, (V*)nullptr));
+        st_stream(reinterpret_cast<V*>(oe + ld + p), packv(tt, (V*)nullptr));
+        if (status) {
+#pragma unroll
+            for (int v = 0; v < W; ++v) status[p + v] = st[v];
+        }
+    }
+}
+
+template <typename S, int MATH>
+__global__ void __launch_bounds__(256)
+k_inv_det_blocks_scalar(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
+                        int64_t begin, int64_t end, int64_t ld, int nblocks) {
+    typedef typename MathT<MATH>::type T;
+    for (int64_t p = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < end;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        T det_all = T(1), t_all = T(1);
+        uint8_t st = 0;
+        for (int b = 0; b < nblocks; ++b) {
+            S x[9];
+            T o[9], det, t;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) x[k] = ld_stream(z + ((int64_t)9 * b + k) * ld + p);
+            uint8_t s1 = solve_core<S, ALGO_ADJ, MATH>(x, o, det, t);
+            st = s1 > st ? s1 : st;
+            det_all = MUL(det_all, det);
+            t_all = MUL(t_all, t);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) st_stream(out + ((int64_t)9 * b + k) * ld + p, (S)o[k]);
+        }
+        st_stream(out + (int64_t)9 * nblocks * ld + p, (S)det_all);
+        st_stream(out + ((int64_t)9 * nblocks + 1) * ld + p, (S)t_all);
+        if (status) status[p] = st;
+    }
+}
+
+template <typename S, int MATH>
+int launch_blocks(const void* zv, void* outv, uint8_t* status, int64_t n, int64_t ld, int nb,
+                  cudaStream_t s) {
+    const S* z = (const S*)zv;
+    S* out = (S*)outv;
+    constexpr int W = Vec<S>::n;
+    bool aligned = ((uintptr_t)z % 16 == 0) && ((uintptr_t)out % 16 == 0) && (ld % W == 0);
+    int64_t n_vec = aligned ? (n / W) * W : 0;
+    if (n_vec > 0) {
+        int64_t groups = n_vec / W;
+        k_inv_det_blocks_vec<S, MATH><<<grid_full(groups, K1_THREADS), K1_THREADS, 0, s>>>(
+            z, out, status, groups, ld, nb);
+    }
+    if (n > n_vec)
+        k_inv_det_blocks_scalar<S, MATH><<<grid_for(n - n_vec, 256), 256, 0, s>>>(z, out, status, n_vec,
+                                                                              n, ld, nb);
+    return launch_check("polsar_inv_det_blocks: launch failed");
 }
 
 template <int ALGO>
@@ -1094,6 +1218,23 @@ int polsar_inv_det(const void* z, void* out, uint8_t* status, int64_t n, int64_t
 int polsar_inv_det_cholesky(const void* z, void* out, uint8_t* status, int64_t n, int64_t ld,
                             int dtype, void* cuda_stream) {
     return dispatch_inv_det<ALGO_CHOL>(z, out, status, n, ld, dtype, cuda_stream);
+}
+
+int polsar_inv_det_blocks(const void* z, void* out, uint8_t* status, int64_t n, int64_t ld,
+                          int nblocks, int dtype, void* cuda_stream) {
+    if (n < 0) return fail(POLSAR_EINVAL, "n < 0");
+    if (ld < n) return fail(POLSAR_EINVAL, "ld < n");
+    if (nblocks < 1 || nblocks > 64) return fail(POLSAR_EINVAL, "nblocks out of [1, 64]");
+    if (n == 0) return POLSAR_OK;
+    if (!z || !out) return fail(POLSAR_EINVAL, "null z or out");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    switch (dtype) {
+        case POLSAR_F32: return launch_blocks<float, MATH_F64>(z, out, status, n, ld, nblocks, s);
+        case POLSAR_F64: return launch_blocks<double, MATH_F64_EFT>(z, out, status, n, ld, nblocks, s);
+        case POLSAR_F32_PLAIN: return launch_blocks<float, MATH_F32>(z, out, status, n, ld, nblocks, s);
+        case POLSAR_F64_PLAIN: return launch_blocks<double, MATH_F64>(z, out, status, n, ld, nblocks, s);
+        default: return fail(POLSAR_EINVAL, "bad dtype");
+    }
 }
 
 size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int dtype) {

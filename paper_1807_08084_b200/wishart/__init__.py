@@ -129,3 +129,23 @@ def cpu_cossin(u: float):
     c, s = ctypes.c_double(), ctypes.c_double()
     _load_cpu().polsar_gen_cpu_cossin(u, ctypes.byref(c), ctypes.byref(s))
     return c.value, s.value
+
+
+def generate_bands(cfg, nbands, device="cuda", stream_stride=100):
+    """Multi-frequency image: nbands independent
+    Wishart images of cfg's law, band b drawn with stream id cfg.stream +
+    b * stream_stride, stacked as 9 * nbands planes (block b at 9b..9b+8)."""
+    import dataclasses
+
+    import torch
+    parts = []
+    for b in range(nbands):
+        cb = dataclasses.replace(cfg, stream=cfg.stream + b * stream_stride)
+        parts.append(generate(cb, device=device))
+    return torch.cat(parts, dim=0).contiguous()
+
+
+def generate_bands_cpu(cfg, nbands, stream_stride=100):
+    import dataclasses
+    return np.concatenate([generate_cpu(dataclasses.replace(cfg, stream=cfg.stream + b * stream_stride))
+                           for b in range(nbands)], axis=0)

@@ -270,3 +270,41 @@ def test_window_power_form_equivalence():
         di, dj = np.linalg.det(full[p]).real, np.linalg.det(full[p + 1]).real
         ds = np.linalg.det((full[p] + full[p + 1]) / 2).real
         assert math.exp(-dij) == pytest.approx(((di / ds) * (dj / ds)) ** 2, rel=1e-12)
+
+
+# ------------------------------------------------- multi-frequency blocks (§V)
+
+def _block_full(z, nb):
+    n = z.shape[1]
+    full = np.zeros((n, 3 * nb, 3 * nb), dtype=np.complex128)
+    for b in range(nb):
+        full[:, 3 * b:3 * b + 3, 3 * b:3 * b + 3] = oracle.to_full(z[9 * b:9 * b + 9])
+    return full
+
+
+@pytest.mark.parametrize("nb", [1, 2, 3, 4])
+def test_blocks_lapack_full_matrix(nb):
+    """The blockwise oracle equals LAPACK on the full 3B x 3B block-diagonal
+    matrix: inverse (every block, and zero off-diagonal blocks by
+    construction) and determinant."""
+    z = np.concatenate([rand_kappa(500, 20 + b, 100.0) for b in range(nb)], axis=0)
+    out = oracle.inv_det_blocks(z, nb)
+    full = _block_full(z, nb)
+    inv = np.linalg.inv(full)
+    det = np.linalg.det(full)
+    for b in range(nb):
+        blk = inv[:, 3 * b:3 * b + 3, 3 * b:3 * b + 3]
+        assert np.all(normwise(out[9 * b:9 * b + 9], pack(blk)) <= 1e-13)
+        # off-diagonal blocks of the LAPACK inverse vanish
+        for c in range(nb):
+            if c != b:
+                assert np.abs(inv[:, 3 * b:3 * b + 3, 3 * c:3 * c + 3]).max() <= 1e-13 * np.abs(inv).max()
+    np.testing.assert_allclose(out[9 * nb], det.real, rtol=1e-13)
+    np.testing.assert_allclose(out[9 * nb + 1], 1 / det.real, rtol=1e-13)
+
+
+def test_blocks_single_block_is_inv_det():
+    z = rand_hpd(300, 30)
+    a = oracle.inv_det_blocks(z, 1)
+    b = oracle.inv_det(z)
+    assert np.array_equal(a, b)
