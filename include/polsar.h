@@ -130,6 +130,20 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
                            int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
                            double h, void* workspace, void* out, int dtype, void* cuda_stream);
 
+/* polsar_nlm_filter -- non-local-means filter output with the same search-
+ * window weights (the NLM filter with stochastic distances of PAPER.md:77-80
+ * [§I]), fused into the window pass:
+ *   W_i = sum_j exp(-d_ij / h),   Zhat_i = sum_j exp(-d_ij / h) Z_j / W_i.
+ * Arguments as polsar_window_distance, plus
+ *   out_w  : device, (e - b) x width values of W, or NULL
+ *   out_z  : device, 9 planes of (e - b) x width filtered pixels (packed
+ *            field order), plane stride ld_out >= (e - b) * width.
+ * Workspace: polsar_window_workspace_bytes(slab_rows, width, dtype). */
+int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
+                      int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
+                      double h, void* workspace, void* out_w, void* out_z, int64_t ld_out,
+                      int dtype, void* cuda_stream);
+
 /* polsar_checksum -- verification reduction (support for multi-GPU
  * bit-identity).  Adds to result[0] (uint64, wrapping)
  * sum_p sum_k mix64(bits(plane k, pixel p) ^ key(pix_offset + p, k)) over

@@ -59,6 +59,8 @@ def lib() -> ctypes.CDLL:
         _lib.oracle_window_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
         _lib.oracle_inv_det_blocks_f64.argtypes = [P, I64, INT, P, I64, I64]
         _lib.oracle_inv_det_blocks_f32.argtypes = [P, I64, INT, P, I64, I64]
+        _lib.oracle_nlm_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+        _lib.oracle_nlm_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
         _lib.oracle_ldbl_mant_dig.restype = INT
         _lib.oracle_quad_mant_dig.restype = INT
     return _lib
@@ -188,6 +190,29 @@ def window(z: np.ndarray, height: int, width: int, radius: int, looks: float,
     fn(_ptr(z), z.shape[1], height, width, int(radius), float(looks), float(h),
        _ptr(idx), idx.shape[0], _ptr(out))
     return out
+
+
+def nlm(z: np.ndarray, height: int, width: int, radius: int, looks: float, h: float, idx=None):
+    """NLM filter output: returns (Zhat (9, m), W (m,)) for pixels idx,
+    Zhat_i = sum_j w_ij Z_j / W_i with the window weights (long double)."""
+    z = _planes(z)
+    if idx is None:
+        idx = np.arange(height * width, dtype=np.int64)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    m = idx.shape[0]
+    out = np.empty((10, m), dtype=np.float64)
+    fn = lib().oracle_nlm_f64 if z.dtype == np.float64 else lib().oracle_nlm_f32
+    fn(_ptr(z), z.shape[1], height, width, int(radius), float(looks), float(h), _ptr(idx), m,
+       _ptr(out))
+    return out[:9], out[9]
+
+
+def nlm_threaded(z, height, width, radius, looks, h, idx, threads):
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    parts = [p for p in np.array_split(idx, threads) if p.size]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = list(ex.map(lambda p: nlm(z, height, width, radius, looks, h, p), parts))
+    return np.concatenate([r[0] for r in res], axis=1), np.concatenate([r[1] for r in res])
 
 
 def window_threaded(z, height, width, radius, looks, h, idx, threads):

@@ -361,6 +361,54 @@ void oracle_window_f32(const float* z, int64_t ld, int64_t height, int64_t width
     }
 }
 
+/* Non-local-means filter output with the window weights (the NLM filter of
+ * PAPER.md:77-80 [§I]):
+ *   W_i = sum_j w_ij,  Zhat_i = sum_j w_ij Z_j / W_i,  w_ij = exp(-d_ij / h),
+ * N(i) the clipped window.  Long double.  out: 10 x m doubles, row q = pixel
+ * idx[q]: out[k*m + q] = Zhat_k (k < 9), out[9*m + q] = W. */
+static void nlm_pixel(herm_ld zi, ld_t looks, ld_t h, const void* z, int is32, int64_t ld,
+                      int64_t height, int64_t width, int radius, int64_t yi, int64_t xi,
+                      ld_t acc[10]) {
+    for (int k = 0; k < 10; ++k) acc[k] = 0.0L;
+    for (int64_t yj = yi - radius; yj <= yi + radius; ++yj) {
+        if (yj < 0 || yj >= height) continue;
+        for (int64_t xj = xi - radius; xj <= xi + radius; ++xj) {
+            if (xj < 0 || xj >= width) continue;
+            herm_ld zj = is32 ? load_ld_f32((const float*)z, ld, yj * width + xj)
+                              : load_ld_f64((const double*)z, ld, yj * width + xj);
+            ld_t w = expl(-pair_distance(zi, zj, looks) / h);
+            acc[0] += w * zj.a;  acc[1] += w * zj.br; acc[2] += w * zj.bi;
+            acc[3] += w * zj.cr; acc[4] += w * zj.ci; acc[5] += w * zj.d;
+            acc[6] += w * zj.er; acc[7] += w * zj.ei; acc[8] += w * zj.f;
+            acc[9] += w;
+        }
+    }
+}
+
+void oracle_nlm_f64(const double* z, int64_t ld, int64_t height, int64_t width, int radius,
+                    double looks, double h, const int64_t* idx, int64_t m, double* out) {
+    for (int64_t q = 0; q < m; ++q) {
+        ld_t acc[10];
+        herm_ld zi = load_ld_f64(z, ld, idx[q]);
+        nlm_pixel(zi, (ld_t)looks, (ld_t)h, z, 0, ld, height, width, radius, idx[q] / width,
+                  idx[q] % width, acc);
+        for (int k = 0; k < 9; ++k) out[k * m + q] = (double)(acc[k] / acc[9]);
+        out[9 * m + q] = (double)acc[9];
+    }
+}
+
+void oracle_nlm_f32(const float* z, int64_t ld, int64_t height, int64_t width, int radius,
+                    double looks, double h, const int64_t* idx, int64_t m, double* out) {
+    for (int64_t q = 0; q < m; ++q) {
+        ld_t acc[10];
+        herm_ld zi = load_ld_f32(z, ld, idx[q]);
+        nlm_pixel(zi, (ld_t)looks, (ld_t)h, z, 1, ld, height, width, radius, idx[q] / width,
+                  idx[q] % width, acc);
+        for (int k = 0; k < 9; ++k) out[k * m + q] = (double)(acc[k] / acc[9]);
+        out[9 * m + q] = (double)acc[9];
+    }
+}
+
 /* Mantissa digits of the evaluation type, so tests can assert the oracle
  * really runs in extended precision on the host it is built on. */
 int oracle_ldbl_mant_dig(void) { return __LDBL_MANT_DIG__; }

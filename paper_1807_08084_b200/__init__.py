@@ -23,7 +23,7 @@ STATUS_OK, STATUS_SINGULAR, STATUS_NOT_PD = 0, 1, 2
 
 __all__ = [
     "polsar_inv_det", "polsar_inv_det_cholesky", "polsar_inv_det_blocks", "polsar_window_distance",
-    "polsar_window_workspace_bytes", "polsar_checksum", "polsar_inv_det_host",
+    "polsar_nlm_filter", "nlm_filter", "polsar_window_workspace_bytes", "polsar_checksum", "polsar_inv_det_host",
     "polsar_host_chunk_pixels", "inv_det", "window_distance", "dtype_code", "PolsarError",
     "POLSAR_F32", "POLSAR_F64", "POLSAR_F32_PLAIN", "POLSAR_F64_PLAIN",
 ]
@@ -158,6 +158,42 @@ def window_distance(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, 
     out = torch.empty((row_end - row_begin) * width, dtype=z.dtype, device=z.device)
     return polsar_window_distance(z, width, height, row_begin, row_end, radius, looks, h, ws, out,
                                   plain=plain, stream=stream)
+
+
+def polsar_nlm_filter(z, width, slab_rows, out_row_begin, out_row_end, radius, looks, h,
+                      workspace, out_z, out_w=None, plain=False, stream=None):
+    """NLM filter output Zhat (9 planes) and optionally W for slab rows
+    [out_row_begin, out_row_end), with the K3 weights."""
+    _dev_check(z, workspace, out_z, out_w)
+    ld = _planes(z, 9)
+    ld_out = _planes(out_z, 9)
+    code = dtype_code(z.dtype, plain)
+    need = polsar_window_workspace_bytes(slab_rows, width, code)
+    if workspace.numel() * workspace.element_size() < need:
+        raise ValueError(f"workspace needs {need} bytes")
+    if out_z.dtype != z.dtype or (out_w is not None and out_w.dtype != z.dtype):
+        raise TypeError("outputs must have the input dtype")
+    rc = lib().polsar_nlm_filter(_ptr(z), ld, width, slab_rows, out_row_begin, out_row_end, radius,
+                                 float(looks), float(h), _ptr(workspace), _ptr(out_w), _ptr(out_z),
+                                 ld_out, code, _stream_ptr(stream))
+    check(rc, "polsar_nlm_filter")
+    return out_z
+
+
+def nlm_filter(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, row_end=None,
+               plain=False, stream=None):
+    """Allocate and run the fused NLM filter on a whole slab; returns (Zhat, W)."""
+    torch = _torch()
+    row_end = height if row_end is None else row_end
+    m = (row_end - row_begin) * width
+    code = dtype_code(z.dtype, plain)
+    ws = torch.empty(polsar_window_workspace_bytes(height, width, code), dtype=torch.uint8,
+                     device=z.device)
+    out_z = torch.empty((9, m), dtype=z.dtype, device=z.device)
+    out_w = torch.empty(m, dtype=z.dtype, device=z.device)
+    polsar_nlm_filter(z, width, height, row_begin, row_end, radius, looks, h, ws, out_z, out_w,
+                      plain=plain, stream=stream)
+    return out_z, out_w
 
 
 def polsar_checksum(planes, n, nplanes, pix_offset=0, status=None, result=None, stream=None):

@@ -827,6 +827,126 @@ int launch_window(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, 
 }
 
 // ------------------------------------------------------------------------
+// K4: non-local-means filter output (the NLM filter with
+// stochastic distances of PAPER.md:77-80 [§I]).  Same pair weights as K3 and
+// in the same pass, accumulated with the window pixels themselves:
+//   W_i = sum_j w_ij,   Zhat_i = sum_j w_ij Z_j / W_i   (9 packed planes).
+// Layout and staging as k_window_sum; the weighted sums accumulate in the
+// pair-determinant type (fp64 for the default modes: one F2F, one DADD and
+// nine DFMA per pair on top of the determinant).
+template <typename S, typename T, typename WT, int TY, int RB>
+__global__ void __launch_bounds__(K3_TX * TY / RB, 1)
+k_nlm_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
+          int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
+          int alpha_is_2, S* __restrict__ out_w, S* __restrict__ out_z, int64_t ld_out) {
+    extern __shared__ unsigned char smem_raw[];
+    const int HW = K3_TX + 2 * R;
+    const int HH = TY + 2 * R;
+    const int HP = HW * HH;
+    T* sz = reinterpret_cast<T*>(smem_raw);
+    WT* sg = reinterpret_cast<WT*>(sz + 9 * HP);
+
+    const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
+    const int64_t y0 = row_begin + (int64_t)blockIdx.y * TY;
+    for (int q = threadIdx.x; q < HP; q += blockDim.x) {
+        int hy = q / HW, hx = q % HW;
+        int64_t gy = y0 - R + hy, gx = x0 - R + hx;
+        bool in = gy >= 0 && gy < slab_rows && gx >= 0 && gx < width;
+        int64_t p = in ? gy * width + gx : 0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) sz[k * HP + q] = in ? (T)z[k * ld + p] : T(0);
+        sg[q] = in ? g[p] : WT(0);
+    }
+    __syncthreads();
+
+    const int tx = threadIdx.x % K3_TX;
+    const int ty0 = (threadIdx.x / K3_TX) * RB;
+    const int64_t gx = x0 + tx;
+    T zi[RB][9], accz[RB][9], accw[RB];
+    WT gi[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        int q = (ty0 + r + R) * HW + (tx + R);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            zi[r][k] = sz[k * HP + q];
+            accz[r][k] = T(0);
+        }
+        gi[r] = sg[q];
+        accw[r] = T(0);
+    }
+    const WT alpha = (WT)alpha_d;
+    const bool a2 = alpha_is_2 != 0;
+    const bool interior_x = (x0 - R >= 0) && (x0 + K3_TX + R <= width);
+
+    for (int wy = -R; wy <= R + RB - 1; ++wy) {
+        const int64_t gyj = y0 + ty0 + wy;
+        if (gyj < 0 || gyj >= slab_rows) continue;  // warp-uniform
+        const int hy = ty0 + wy + R;
+        const T* rowz = sz + hy * HW + tx + R;
+        const WT* rowg = sg + hy * HW + tx + R;
+        bool rok[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) rok[r] = (wy - r >= -R) && (wy - r <= R);  // warp-uniform
+        for (int wx = -R; wx <= R; ++wx) {
+            T zj[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
+            const WT gj = rowg[wx];
+            const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                if (rok[r]) {
+                    WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
+                    const T wt = colok ? (T)w : T(0);
+                    accw[r] = ADD(accw[r], wt);
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) accz[r][k] = FMA(wt, zj[k], accz[r][k]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        const int64_t gy = y0 + ty0 + r;
+        if (gx < width && gy < row_end) {
+            const int64_t o = (gy - row_begin) * width + gx;
+            if (out_w) out_w[o] = (S)accw[r];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) out_z[k * ld_out + o] = (S)(accz[r][k] / accw[r]);
+        }
+    }
+}
+
+template <typename S, typename T, typename WT>
+int launch_nlm(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re,
+               int R, double looks, double h, void* ws, void* out_w, void* out_z, int64_t ld_out,
+               cudaStream_t s) {
+    const S* z = (const S*)zv;
+    WT* g = (WT*)ws;
+    const int64_t n = slab_rows * width;
+    k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
+    const double alpha = looks / (2.0 * h);
+    dim3 block(K3_TX * 16 / 2);
+    int TY = 16;
+    size_t smem = window_smem<T, WT>(16, R);
+    if (smem > K3_SMEM_MAX) {
+        TY = 8;
+        smem = window_smem<T, WT>(8, R);
+        if (smem > K3_SMEM_MAX)
+            return fail(POLSAR_ENOTSUP, "polsar_nlm_filter: radius too large for shared memory");
+    }
+    auto kern = TY == 16 ? k_nlm_sum<S, T, WT, 16, 2> : k_nlm_sum<S, T, WT, 8, 2>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return fail(POLSAR_ENOTSUP, "polsar_nlm_filter: shared memory request too large");
+    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - rb + TY - 1) / TY));
+    kern<<<grid, K3_TX * TY / 2, smem, s>>>(z, ld, width, slab_rows, rb, re, R, g, alpha,
+                                            alpha == 2.0 ? 1 : 0, (S*)out_w, (S*)out_z, ld_out);
+    return launch_check("polsar_nlm_filter: launch failed");
+}
+
+// ------------------------------------------------------------------------
 // K3 (v3, the fp64-determinant modes): the pair determinant by the 3x3
 // expansion  det(A + B) = det A + det B + <adj A, B> + <A, adj B>,
 // <X, Y> = tr(X Y) = sum_k w_k x_k y_k over the packed components with
@@ -1274,6 +1394,36 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
         case POLSAR_F32_PLAIN:
             return launch_window<float, float, float>(z, ld, width, slab_rows, out_row_begin,
                                                       out_row_end, radius, looks, h, workspace, out, s);
+        default: return fail(POLSAR_EINVAL, "bad dtype");
+    }
+}
+
+int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
+                      int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
+                      double h, void* workspace, void* out_w, void* out_z, int64_t ld_out,
+                      int dtype, void* cuda_stream) {
+    if (width < 0 || slab_rows < 0) return fail(POLSAR_EINVAL, "negative size");
+    if (out_row_begin < 0 || out_row_end < out_row_begin || out_row_end > slab_rows)
+        return fail(POLSAR_EINVAL, "bad output row range");
+    if (radius < 0 || radius > 16) return fail(POLSAR_EINVAL, "radius out of [0, 16]");
+    if (!(looks > 0) || !(h > 0)) return fail(POLSAR_EINVAL, "looks and h must be > 0");
+    if (ld < slab_rows * width) return fail(POLSAR_EINVAL, "ld < slab_rows*width");
+    if (ld_out < (out_row_end - out_row_begin) * width) return fail(POLSAR_EINVAL, "ld_out too small");
+    if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
+    if (!z || !workspace || !out_z) return fail(POLSAR_EINVAL, "null pointer");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    switch (dtype) {
+        case POLSAR_F32:
+            return launch_nlm<float, double, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                    radius, looks, h, workspace, out_w, out_z, ld_out, s);
+        case POLSAR_F64:
+        case POLSAR_F64_PLAIN:
+            return launch_nlm<double, double, double>(z, ld, width, slab_rows, out_row_begin,
+                                                      out_row_end, radius, looks, h, workspace, out_w,
+                                                      out_z, ld_out, s);
+        case POLSAR_F32_PLAIN:
+            return launch_nlm<float, float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                   radius, looks, h, workspace, out_w, out_z, ld_out, s);
         default: return fail(POLSAR_EINVAL, "bad dtype");
     }
 }

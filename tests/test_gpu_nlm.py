@@ -1,0 +1,62 @@
+"""Fused NLM filter output: Zhat and W
+against the long-double oracle, closed forms and slab decomposition."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1807_08084_b200 as P
+from paper_1807_08084_b200 import configs, wishart
+
+pytestmark = pytest.mark.gpu
+THREADS = len(os.sched_getaffinity(0))
+# fp32 storage: BASELINE's 2e-5 (normwise over the 9 components of Zhat_i);
+# fp64: the weight error bound of test_gpu_window (4e-10)
+TOL = {torch.float32: 2e-5, torch.float64: 4e-10}
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 53), 3), ((40, 45), 14)])
+def test_nlm_parity(cuda, dt, shape, radius):
+    h, w = shape
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda).to(dt)
+    zhat, W = P.nlm_filter(z, h, w, radius=radius)
+    zh = z.cpu().numpy()
+    rz, rw = oracle.nlm_threaded(zh, h, w, radius, 4.0, 1.0, np.arange(h * w), THREADS)
+    got = zhat.cpu().numpy().astype(np.float64)
+    err = np.max(np.abs(got - rz), axis=0) / np.max(np.abs(rz), axis=0)
+    assert err.max() <= TOL[dt], err.max()
+    werr = np.abs(W.cpu().numpy() - rw) / rw
+    assert werr.max() <= TOL[dt], werr.max()
+
+
+def test_nlm_w_matches_window(cuda):
+    h, w = 120, 100
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda)
+    _, W = P.nlm_filter(z, h, w)
+    W2 = P.window_distance(z, h, w)
+    rel = ((W.double() - W2.double()).abs() / W2.double()).max().item()
+    assert rel <= 2e-5
+
+
+def test_nlm_constant_image(cuda):
+    h, w = 50, 70
+    z1 = wishart.generate(configs.get("c5").scaled(1, 1), device=cuda).double()
+    z = z1.repeat(1, h * w).contiguous()
+    zhat, _ = P.nlm_filter(z, h, w)
+    assert torch.allclose(zhat, z, rtol=1e-14, atol=0)
+
+
+def test_nlm_slab_consistency(cuda):
+    h, w, r = 150, 64, 11
+    cfg = configs.get("c5").scaled(h, w)
+    z = wishart.generate(cfg, device=cuda)
+    full, fw = P.nlm_filter(z, h, w, radius=r)
+    for r0, r1 in ((0, 40), (40, 111), (111, 150)):
+        s0, s1 = max(0, r0 - r), min(h, r1 + r)
+        slab = wishart.generate(cfg, s0, s1, device=cuda)
+        part, pw = P.nlm_filter(slab, s1 - s0, w, radius=r, row_begin=r0 - s0, row_end=r1 - s0)
+        assert torch.equal(part, full[:, r0 * w:r1 * w])
+        assert torch.equal(pw, fw[r0 * w:r1 * w])

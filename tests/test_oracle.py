@@ -308,3 +308,58 @@ def test_blocks_single_block_is_inv_det():
     a = oracle.inv_det_blocks(z, 1)
     b = oracle.inv_det(z)
     assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- NLM oracle
+
+def test_nlm_constant_image():
+    h, w, r = 7, 9, 3
+    z0 = rand_hpd(1, 40)[:, 0]
+    z = np.repeat(z0[:, None], h * w, axis=1)
+    zhat, W = oracle.nlm(z, h, w, r, 4.0, 1.0)
+    np.testing.assert_allclose(zhat, z, rtol=1e-15, atol=1e-15 * np.abs(z0).max())
+    ref = np.array([clipped_count(p // w, p % w, h, w, r) for p in range(h * w)], float)
+    assert np.array_equal(W, ref)
+
+
+def test_nlm_two_class_closed_form():
+    h, w, r, looks = 6, 10, 2, 4.0
+    za, zb = rand_hpd(2, 41)[:, 0], rand_hpd(2, 41)[:, 1]
+    xs = np.arange(h * w) % w
+    z = np.where(xs[None, :] < 5, za[:, None], zb[:, None])
+    zhat, W = oracle.nlm(z, h, w, r, looks, 1.0)
+    fa, fb = oracle.to_full(za[:, None])[0], oracle.to_full(zb[:, None])[0]
+    dab = looks * (np.linalg.slogdet((fa + fb) / 2)[1]
+                   - 0.5 * (np.linalg.slogdet(fa)[1] + np.linalg.slogdet(fb)[1]))
+    e = math.exp(-dab)
+    for p in range(h * w):
+        y, x = divmod(p, w)
+        ys = range(max(0, y - r), min(h, y + r + 1))
+        xr = range(max(0, x - r), min(w, x + r + 1))
+        same = sum(1 for _ in ys for xx in xr if (xx < 5) == (x < 5))
+        other = len(ys) * len(xr) - same
+        zs, zo = (za, zb) if x < 5 else (zb, za)
+        ref = (same * zs + other * e * zo) / (same + other * e)
+        np.testing.assert_allclose(zhat[:, p], ref, rtol=1e-12, atol=1e-13)
+        assert W[p] == pytest.approx(same + other * e, rel=1e-13)
+
+
+def test_nlm_brute_force_tiny():
+    h, w, r, looks, hh = 4, 5, 1, 4.0, 1.0
+    z = rand_kappa(h * w, 42, 30.0)
+    zhat, W = oracle.nlm(z, h, w, r, looks, hh)
+    full = oracle.to_full(z)
+    ld = np.log(np.linalg.det(full).real)
+    for p in range(h * w):
+        y, x = divmod(p, w)
+        num = np.zeros(9)
+        den = 0.0
+        for yy in range(max(0, y - r), min(h, y + r + 1)):
+            for xx in range(max(0, x - r), min(w, x + r + 1)):
+                q = yy * w + xx
+                ds = np.log(np.linalg.det((full[p] + full[q]) / 2).real)
+                wq = math.exp(-looks * (ds - 0.5 * (ld[p] + ld[q])) / hh)
+                num += wq * z[:, q]
+                den += wq
+        np.testing.assert_allclose(zhat[:, p], num / den, rtol=1e-11, atol=1e-12)
+        assert W[p] == pytest.approx(den, rel=1e-12)

@@ -54,6 +54,13 @@ def main():
             ws = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, 1),
                              dtype=torch.uint8, device=dev)
             out = torch.empty(c5.n, dtype=z64.dtype, device=dev)
+            zz = torch.empty((9, c5.n), dtype=z.dtype, device=dev)
+            wo = torch.empty(c5.n, dtype=z.dtype, device=dev)
+            ws32 = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, 0),
+                               dtype=torch.uint8, device=dev)
+            res["nlm_c5_ms"] = timeit(lambda: P.polsar_nlm_filter(z, c5.width, c5.height, 0, c5.height,
+                                                                  c5.radius, c5.looks, c5.h, ws32, zz, wo,
+                                                                  stream=s), s, steps=3)
             res["window_c5_fp64_ms"] = timeit(lambda: P.polsar_window_distance(
                 z64, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, out,
                 stream=s), s, steps=3)
