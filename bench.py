@@ -150,6 +150,20 @@ def bytes_per_matrix(esz, status):
     return 20 * esz + (1 if status else 0)
 
 
+def config_dict(cfg, args, world, n, H, status_plane, bpm, flushed):
+    """The `config` object both arms print (same workload description)."""
+    return {
+        "workload": f"{cfg.name}: BASELINE configs[{cfg.baseline_index}] "
+                    f"{cfg.height}x{cfg.width} {cfg.dtype} L={cfg.looks} per GPU",
+        "algo": "Alg. 2 (adjugate)" if args.algo == "adjugate" else "Alg. 1 (Cholesky, l21 fixed)",
+        "storage": cfg.dtype, "mode": "plain" if args.plain else "default",
+        "pixels_per_gpu": n, "image_rows": H, "status_plane": status_plane,
+        "l2": "flushed between steps" if flushed else
+              f"inputs+outputs {n * bpm / 1e9:.1f} GB per step >> 126 MB L2 (no flush)",
+        "parallelism": f"dp{world} (pixel rows)",
+    }
+
+
 # ------------------------------------------------------------ reference arm
 def run_reference(args):
     """The CPU oracle (oracle/, as it stands) on the host cores, on a bounded
@@ -163,6 +177,8 @@ def run_reference(args):
     from paper_1807_08084_b200 import configs, wishart
 
     cfg = configs.get(args.config)
+    if args.rows:
+        cfg = cfg.scaled(args.rows)
     cores = len(os.sched_getaffinity(0))
     sample = min(cfg.n, 1 << 22)  # 4.2M matrices per step (~0.3-0.6 s on 16 cores)
     rows = max(1, sample // cfg.width)
@@ -182,8 +198,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "binary128 (oracle)", "data": "synthetic (seeded Wishart, host twin generator)",
-        "config": {"workload": f"{cfg.name} (BASELINE configs[{cfg.baseline_index}]) bounded sample",
-                   "sample_pixels": sample, "looks": cfg.looks, "storage": cfg.dtype},
+        "config": dict(config_dict(cfg, args, world, cfg.n, cfg.height * (world if args.scaling == "weak" else 1),
+                                   not args.no_status, bytes_per_matrix(4 if cfg.dtype == "float32" else 8,
+                                                                        not args.no_status), False),
+                       sample_pixels_per_step=sample),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"first {sample} pixels of {cfg.name}, per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -283,16 +301,7 @@ def run_ours(args):
         "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32" if (args.plain and tdt == torch.float32) else "f64",
         "data": "synthetic (seeded Wishart, BASELINE law)",
-        "config": {
-            "workload": f"{cfg.name}: BASELINE configs[{cfg.baseline_index}] "
-                        f"{cfg.height}x{cfg.width} {cfg.dtype} L={cfg.looks} per GPU",
-            "algo": "Alg. 2 (adjugate)" if args.algo == "adjugate" else "Alg. 1 (Cholesky, l21 fixed)",
-            "storage": cfg.dtype, "mode": "plain" if args.plain else "default",
-            "pixels_per_gpu": n, "image_rows": H, "status_plane": status is not None,
-            "l2": "flushed between steps" if l2_flush is not None else
-                  f"inputs+outputs {n * bpm / 1e9:.1f} GB per step >> 126 MB L2 (no flush)",
-            "parallelism": f"dp{world} (pixel rows)",
-        },
+        "config": config_dict(cfg, args, world, n, H, status is not None, bpm, l2_flush is not None),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src, "bytes_per_matrix": bpm},
