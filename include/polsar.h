@@ -130,6 +130,19 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
                            int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
                            double h, void* workspace, void* out, int dtype, void* cuda_stream);
 
+/* polsar_window_kl -- the same window sum with the symmetric Wishart
+ * Kullback-Leibler distance (one of the divergences that need Z^-1, PAPER.md:
+ * 70-76 [§I]):
+ *   d_ij = L [ (tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i)) / 2 - 3 ],  W_i = sum_j exp(-d_ij / h).
+ * Z^-1 of every slab pixel comes from Alg. 2 (K1's device function) in a
+ * prepass; each pair is then two 9-term trace products in fp64.  Arguments,
+ * workspace (polsar_window_workspace_bytes) and errors as
+ * polsar_window_distance; radius <= 12; dtype POLSAR_F32 or POLSAR_F64
+ * (POLSAR_F32_PLAIN returns ENOTSUP). */
+int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
+                     int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
+                     double h, void* workspace, void* out, int dtype, void* cuda_stream);
+
 /* polsar_nlm_filter -- non-local-means filter output with the same search-
  * window weights (the NLM filter with stochastic distances of PAPER.md:77-80
  * [§I]), fused into the window pass:

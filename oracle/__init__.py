@@ -61,6 +61,10 @@ def lib() -> ctypes.CDLL:
         _lib.oracle_inv_det_blocks_f32.argtypes = [P, I64, INT, P, I64, I64]
         _lib.oracle_nlm_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
         _lib.oracle_nlm_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+        _lib.oracle_window_kl_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+        _lib.oracle_window_kl_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+        _lib.oracle_kl_distance.argtypes = [P, P, D]
+        _lib.oracle_kl_distance.restype = D
         _lib.oracle_ldbl_mant_dig.restype = INT
         _lib.oracle_quad_mant_dig.restype = INT
     return _lib
@@ -190,6 +194,34 @@ def window(z: np.ndarray, height: int, width: int, radius: int, looks: float,
     fn(_ptr(z), z.shape[1], height, width, int(radius), float(looks), float(h),
        _ptr(idx), idx.shape[0], _ptr(out))
     return out
+
+
+def kl_distance(zi, zj, looks: float) -> float:
+    """Symmetric Wishart KL distance L[(tr(Zi^-1 Zj) + tr(Zj^-1 Zi))/2 - 3]."""
+    zi = np.ascontiguousarray(zi, dtype=np.float64).reshape(9)
+    zj = np.ascontiguousarray(zj, dtype=np.float64).reshape(9)
+    return lib().oracle_kl_distance(_ptr(zi), _ptr(zj), float(looks))
+
+
+def window_kl(z, height, width, radius, looks, h, idx=None):
+    """W_i with the symmetric Wishart KL distance (long double)."""
+    z = _planes(z)
+    if idx is None:
+        idx = np.arange(height * width, dtype=np.int64)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    out = np.empty(idx.shape[0], dtype=np.float64)
+    fn = lib().oracle_window_kl_f64 if z.dtype == np.float64 else lib().oracle_window_kl_f32
+    fn(_ptr(z), z.shape[1], height, width, int(radius), float(looks), float(h), _ptr(idx),
+       idx.shape[0], _ptr(out))
+    return out
+
+
+def window_kl_threaded(z, height, width, radius, looks, h, idx, threads):
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    parts = [p for p in np.array_split(idx, threads) if p.size]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = list(ex.map(lambda p: window_kl(z, height, width, radius, looks, h, p), parts))
+    return np.concatenate(res)
 
 
 def nlm(z: np.ndarray, height: int, width: int, radius: int, looks: float, h: float, idx=None):

@@ -361,6 +361,80 @@ void oracle_window_f32(const float* z, int64_t ld, int64_t height, int64_t width
     }
 }
 
+/* Window sum with the symmetric Wishart Kullback-Leibler distance (the
+ * divergences of PAPER.md:70-76 [§I] that need Z^-1):
+ *   d_ij = L [ (tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i)) / 2 - 3 ],  W_i = sum_j exp(-d_ij / h).
+ * Z^-1 by the cofactor definition (Eq. 3/4), traces by the plain definition
+ * tr(X Y) = sum_k sum_l X_kl Y_lk over the full complex 3x3 matrices; long
+ * double. */
+typedef struct { ld_t re, im; } cld;
+
+static void full_ld(herm_ld m, cld M[3][3]) {
+    M[0][0].re = m.a;  M[0][0].im = 0;
+    M[1][1].re = m.d;  M[1][1].im = 0;
+    M[2][2].re = m.f;  M[2][2].im = 0;
+    M[0][1].re = m.br; M[0][1].im = m.bi;  M[1][0].re = m.br; M[1][0].im = -m.bi;
+    M[0][2].re = m.cr; M[0][2].im = m.ci;  M[2][0].re = m.cr; M[2][0].im = -m.ci;
+    M[1][2].re = m.er; M[1][2].im = m.ei;  M[2][1].re = m.er; M[2][1].im = -m.ei;
+}
+
+static herm_ld inverse_ld(herm_ld m) {
+    herm_ld c = cofactors_ld(m), x;
+    ld_t re, im;
+    det_full_ld(m, c, &re, &im);
+    x.a = c.a / re;   x.br = c.br / re; x.bi = c.bi / re; x.cr = c.cr / re; x.ci = c.ci / re;
+    x.d = c.d / re;   x.er = c.er / re; x.ei = c.ei / re; x.f = c.f / re;
+    return x;
+}
+
+static ld_t trace_prod(herm_ld x, herm_ld y) {
+    cld X[3][3], Y[3][3];
+    full_ld(x, X);
+    full_ld(y, Y);
+    ld_t t = 0;  /* real part of sum_k sum_l X_kl Y_lk (the trace is real) */
+    for (int k = 0; k < 3; ++k)
+        for (int l = 0; l < 3; ++l) t += X[k][l].re * Y[l][k].re - X[k][l].im * Y[l][k].im;
+    return t;
+}
+
+static void window_kl_any(const void* z, int is32, int64_t ld, int64_t height, int64_t width,
+                          int radius, double looks, double h, const int64_t* idx, int64_t m,
+                          double* out) {
+    for (int64_t q = 0; q < m; ++q) {
+        int64_t yi = idx[q] / width, xi = idx[q] % width;
+        herm_ld zi = is32 ? load_ld_f32((const float*)z, ld, idx[q]) : load_ld_f64((const double*)z, ld, idx[q]);
+        herm_ld xinv = inverse_ld(zi);
+        ld_t acc = 0.0L;
+        for (int64_t yj = yi - radius; yj <= yi + radius; ++yj) {
+            if (yj < 0 || yj >= height) continue;
+            for (int64_t xj = xi - radius; xj <= xi + radius; ++xj) {
+                if (xj < 0 || xj >= width) continue;
+                int64_t pj = yj * width + xj;
+                herm_ld zj = is32 ? load_ld_f32((const float*)z, ld, pj) : load_ld_f64((const double*)z, ld, pj);
+                ld_t d = (ld_t)looks * ((trace_prod(xinv, zj) + trace_prod(inverse_ld(zj), zi)) / 2.0L - 3.0L);
+                acc += expl(-d / (ld_t)h);
+            }
+        }
+        out[q] = (double)acc;
+    }
+}
+
+void oracle_window_kl_f64(const double* z, int64_t ld, int64_t height, int64_t width, int radius,
+                          double looks, double h, const int64_t* idx, int64_t m, double* out) {
+    window_kl_any(z, 0, ld, height, width, radius, looks, h, idx, m, out);
+}
+
+void oracle_window_kl_f32(const float* z, int64_t ld, int64_t height, int64_t width, int radius,
+                          double looks, double h, const int64_t* idx, int64_t m, double* out) {
+    window_kl_any(z, 1, ld, height, width, radius, looks, h, idx, m, out);
+}
+
+/* d_KL for two packed matrices (9 doubles each). */
+double oracle_kl_distance(const double* zi9, const double* zj9, double looks) {
+    herm_ld x = load_ld_f64(zi9, 1, 0), y = load_ld_f64(zj9, 1, 0);
+    return (double)((ld_t)looks * ((trace_prod(inverse_ld(x), y) + trace_prod(inverse_ld(y), x)) / 2.0L - 3.0L));
+}
+
 /* Non-local-means filter output with the window weights (the NLM filter of
  * PAPER.md:77-80 [§I]):
  *   W_i = sum_j w_ij,  Zhat_i = sum_j w_ij Z_j / W_i,  w_ij = exp(-d_ij / h),

@@ -23,7 +23,7 @@ STATUS_OK, STATUS_SINGULAR, STATUS_NOT_PD = 0, 1, 2
 
 __all__ = [
     "polsar_inv_det", "polsar_inv_det_cholesky", "polsar_inv_det_blocks", "polsar_window_distance",
-    "polsar_nlm_filter", "nlm_filter", "polsar_window_workspace_bytes", "polsar_checksum", "polsar_inv_det_host",
+    "polsar_nlm_filter", "nlm_filter", "polsar_window_kl", "window_kl", "polsar_window_workspace_bytes", "polsar_checksum", "polsar_inv_det_host",
     "polsar_host_chunk_pixels", "inv_det", "window_distance", "dtype_code", "PolsarError",
     "POLSAR_F32", "POLSAR_F64", "POLSAR_F32_PLAIN", "POLSAR_F64_PLAIN",
 ]
@@ -158,6 +158,36 @@ def window_distance(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, 
     out = torch.empty((row_end - row_begin) * width, dtype=z.dtype, device=z.device)
     return polsar_window_distance(z, width, height, row_begin, row_end, radius, looks, h, ws, out,
                                   plain=plain, stream=stream)
+
+
+def polsar_window_kl(z, width, slab_rows, out_row_begin, out_row_end, radius, looks, h,
+                     workspace, out, stream=None):
+    """Window sum with the symmetric Wishart KL distance."""
+    _dev_check(z, workspace, out)
+    ld = _planes(z, 9)
+    code = dtype_code(z.dtype)
+    need = polsar_window_workspace_bytes(slab_rows, width, code)
+    if workspace.numel() * workspace.element_size() < need:
+        raise ValueError(f"workspace needs {need} bytes")
+    if out.numel() < (out_row_end - out_row_begin) * width or out.dtype != z.dtype:
+        raise ValueError("out too small or wrong dtype")
+    rc = lib().polsar_window_kl(_ptr(z), ld, width, slab_rows, out_row_begin, out_row_end, radius,
+                                float(looks), float(h), _ptr(workspace), _ptr(out), code,
+                                _stream_ptr(stream))
+    check(rc, "polsar_window_kl")
+    return out
+
+
+def window_kl(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, row_end=None,
+              stream=None):
+    torch = _torch()
+    row_end = height if row_end is None else row_end
+    code = dtype_code(z.dtype)
+    ws = torch.empty(polsar_window_workspace_bytes(height, width, code), dtype=torch.uint8,
+                     device=z.device)
+    out = torch.empty((row_end - row_begin) * width, dtype=z.dtype, device=z.device)
+    return polsar_window_kl(z, width, height, row_begin, row_end, radius, looks, h, ws, out,
+                            stream=stream)
 
 
 def polsar_nlm_filter(z, width, slab_rows, out_row_begin, out_row_end, radius, looks, h,

@@ -978,6 +978,39 @@ constexpr int V3_XOFF = V3_RMAX; // column of x0 inside a staged row (even)
 constexpr int V3_SW = V3_TX + 2 * V3_XOFF;  // staged row width (compile-time strides)
 constexpr int V3_CHP = V3_CH * V3_SW;       // pixels per chunk plane
 
+// KL prepass: planes 9..17 hold w * Z^-1 from Alg. 2
+// (K1's device function: cofactors, Eq. 6 det, t = 1/det, scale), plane 18
+// holds 0, so the pair sum T = <X_i, Z_j> + <Z_i, X_j> = tr(Z_i^-1 Z_j) +
+// tr(Z_j^-1 Z_i).
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_window_prep_kl(const S* __restrict__ z, int64_t ld, int64_t n, double* __restrict__ ws) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        H9<double> m;
+        m.a = (double)z[0 * ld + p];
+        m.br = (double)z[1 * ld + p];
+        m.bi = (double)z[2 * ld + p];
+        m.cr = (double)z[3 * ld + p];
+        m.ci = (double)z[4 * ld + p];
+        m.d = (double)z[5 * ld + p];
+        m.er = (double)z[6 * ld + p];
+        m.ei = (double)z[7 * ld + p];
+        m.f = (double)z[8 * ld + p];
+        double x[9], det, t;
+        alg2_plain<double>(m, x, det, t);
+        const int64_t P = n;
+        ws[0 * P + p] = m.a;  ws[1 * P + p] = m.br; ws[2 * P + p] = m.bi;
+        ws[3 * P + p] = m.cr; ws[4 * P + p] = m.ci; ws[5 * P + p] = m.d;
+        ws[6 * P + p] = m.er; ws[7 * P + p] = m.ei; ws[8 * P + p] = m.f;
+        const double wk[9] = {1, 2, 2, 2, 2, 1, 2, 2, 1};
+#pragma unroll
+        for (int k = 0; k < 9; ++k) ws[(9 + k) * P + p] = wk[k] * x[k];
+        ws[18 * P + p] = 0.0;
+        ws[19 * P + p] = 0.0;
+    }
+}
+
 template <typename S, typename WT>
 __global__ void __launch_bounds__(256)
 k_window_prep_v3(const S* __restrict__ z, int64_t ld, int64_t n, double* __restrict__ ws) {
@@ -1043,6 +1076,21 @@ __device__ __forceinline__ float load_g<float>(double v) {
 template <>
 __device__ __forceinline__ double load_g<double>(double v) { return v; }
 
+// Weight of a pair for the symmetric Wishart KL distance:
+// T = tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i), d = L (T/2 - 3), w = exp(-d/h);
+// lk = L/h.  The subtraction is done in fp64 (T/2 ~ 3 for similar pixels).
+template <typename WT>
+__device__ __forceinline__ WT weight_kl(double T, WT lk);
+template <>
+__device__ __forceinline__ float weight_kl<float>(double T, float lk) {
+    const float d = (float)__fma_rn(T, 0.5, -3.0);
+    return fast_exp2(-lk * d * 1.4426950408889634f);
+}
+template <>
+__device__ __forceinline__ double weight_kl<double>(double T, double lk) {
+    return exp(-lk * __fma_rn(T, 0.5, -3.0));
+}
+
 template <typename WT>
 __device__ __forceinline__ WT weight_v3(double T, WT gi, WT gj, WT alpha, bool a2) {
     WT ft = (WT)T;
@@ -1100,7 +1148,17 @@ __device__ __forceinline__ void pair_T_block(const double (&ui)[RB][9], const do
     for (int r = 0; r < RB; ++r) T[r] = __dadd_rn(A[r], B[r]);
 }
 
-template <typename S, typename WT, bool A2>
+enum { DIST_LOGDET = 0, DIST_KL = 1 };
+
+template <int KIND, typename WT>
+__device__ __forceinline__ WT weight_kind(double T, WT gi, WT gj, WT alpha, bool a2) {
+    if constexpr (KIND == DIST_KL)
+        return weight_kl<WT>(T, alpha);
+    else
+        return weight_v3<WT>(T, gi, gj, alpha, a2);
+}
+
+template <typename S, typename WT, bool A2, int KIND = DIST_LOGDET>
 __global__ void __launch_bounds__(V3_THREADS, 1)
 k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows, int64_t row_begin,
                 int64_t row_end, int R, double alpha_d, S* __restrict__ out) {
@@ -1203,7 +1261,7 @@ k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows,
                     pair_T_block<V3_RB>(ui, zi, Di, uj, zj, Dj, T);
 #pragma unroll
                     for (int r = 0; r < V3_RB; ++r) {
-                        WT w = weight_v3<WT>(Tp[r], gi[r], gp, alpha, a2);
+                        WT w = weight_kind<KIND, WT>(Tp[r], gi[r], gp, alpha, a2);
                         rowacc[r] += okp ? w : WT(0);
                         Tp[r] = T[r];
                     }
@@ -1212,7 +1270,7 @@ k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows,
                 }
 #pragma unroll
                 for (int r = 0; r < V3_RB; ++r) {
-                    WT w = weight_v3<WT>(Tp[r], gi[r], gp, alpha, a2);
+                    WT w = weight_kind<KIND, WT>(Tp[r], gi[r], gp, alpha, a2);
                     rowacc[r] += okp ? w : WT(0);
                 }
             } else {
@@ -1231,7 +1289,7 @@ k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows,
                     for (int r = 0; r < V3_RB; ++r) {
                         const int dy = dy0 - r;
                         if (dy >= -R && dy <= R) {  // CTA-uniform
-                            WT w = weight_v3<WT>(pair_T(ui[r], zi[r], Di[r], uj, zj, Dj), gi[r], gj, alpha, a2);
+                            WT w = weight_kind<KIND, WT>(pair_T(ui[r], zi[r], Di[r], uj, zj, Dj), gi[r], gj, alpha, a2);
                             rowacc[r] += colok ? w : WT(0);
                         }
                     }
@@ -1265,6 +1323,23 @@ int launch_window_v3(const void* zv, int64_t ld, int64_t width, int64_t slab_row
     dim3 grid((unsigned)((width + V3_TX - 1) / V3_TX), (unsigned)((re - rb + V3_RB - 1) / V3_RB));
     kern<<<grid, V3_THREADS, smem, s>>>(ws, width, slab_rows, rb, re, R, alpha, (S*)outv);
     return launch_check("polsar_window_distance: launch failed");
+}
+
+template <typename S, typename WT>
+int launch_window_kl(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
+                     int64_t re, int R, double looks, double h, void* wsv, void* outv,
+                     cudaStream_t s) {
+    const int64_t n = slab_rows * width;
+    double* ws = (double*)wsv;
+    k_window_prep_kl<S><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, ws);
+    size_t smem = (size_t)2 * V3_NP * V3_CHP * sizeof(double);
+    auto kern = k_window_sum_v3<S, WT, false, DIST_KL>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return fail(POLSAR_ENOTSUP, "polsar_window_kl: shared memory request too large");
+    dim3 grid((unsigned)((width + V3_TX - 1) / V3_TX), (unsigned)((re - rb + V3_RB - 1) / V3_RB));
+    kern<<<grid, V3_THREADS, smem, s>>>(ws, width, slab_rows, rb, re, R, looks / h, (S*)outv);
+    return launch_check("polsar_window_kl: launch failed");
 }
 
 // ======================================================= R1: checksums
@@ -1395,6 +1470,30 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
             return launch_window<float, float, float>(z, ld, width, slab_rows, out_row_begin,
                                                       out_row_end, radius, looks, h, workspace, out, s);
         default: return fail(POLSAR_EINVAL, "bad dtype");
+    }
+}
+
+int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
+                     int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
+                     double h, void* workspace, void* out, int dtype, void* cuda_stream) {
+    if (width < 0 || slab_rows < 0) return fail(POLSAR_EINVAL, "negative size");
+    if (out_row_begin < 0 || out_row_end < out_row_begin || out_row_end > slab_rows)
+        return fail(POLSAR_EINVAL, "bad output row range");
+    if (radius < 0 || radius > V3_RMAX) return fail(POLSAR_EINVAL, "radius out of [0, 12]");
+    if (!(looks > 0) || !(h > 0)) return fail(POLSAR_EINVAL, "looks and h must be > 0");
+    if (ld < slab_rows * width) return fail(POLSAR_EINVAL, "ld < slab_rows*width");
+    if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
+    if (!z || !workspace || !out) return fail(POLSAR_EINVAL, "null pointer");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    switch (dtype) {
+        case POLSAR_F32:
+            return launch_window_kl<float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                  radius, looks, h, workspace, out, s);
+        case POLSAR_F64:
+        case POLSAR_F64_PLAIN:
+            return launch_window_kl<double, double>(z, ld, width, slab_rows, out_row_begin,
+                                                    out_row_end, radius, looks, h, workspace, out, s);
+        default: return fail(POLSAR_ENOTSUP, "polsar_window_kl: fp32-arithmetic mode not provided");
     }
 }
 

@@ -1,0 +1,52 @@
+"""Window sum with the symmetric Wishart KL distance,
+Z^-1 of every pixel from Alg. 2: GPU against the long-double oracle."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1807_08084_b200 as P
+from paper_1807_08084_b200 import configs, wishart
+
+pytestmark = pytest.mark.gpu
+THREADS = len(os.sched_getaffinity(0))
+# fp32 storage: 2e-5 as for K3.  fp64: the two trace products carry ~81 kappa u
+# relative error each, the weight multiplies the absolute error of d by w:
+# L * 2 * 81 * 1e4 * 2^-53 * |T| ~ 1e-9 at kappa <= 1e4.
+TOL = {torch.float32: 2e-5, torch.float64: 2e-9}
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 290), 3), ((20, 70), 0)])
+def test_window_kl_parity(cuda, dt, shape, radius):
+    h, w = shape
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda).to(dt)
+    got = P.window_kl(z, h, w, radius=radius).cpu().numpy()
+    ref = oracle.window_kl_threaded(z.cpu().numpy(), h, w, radius, 4.0, 1.0, np.arange(h * w), THREADS)
+    rel = np.abs(got - ref) / ref
+    assert rel.max() <= TOL[dt], rel.max()
+
+
+def test_window_kl_constant_image(cuda):
+    h, w, r = 40, 300, 11
+    z1 = wishart.generate(configs.get("c5").scaled(1, 1), device=cuda)
+    z = z1.repeat(1, h * w).contiguous()
+    got = P.window_kl(z, h, w, radius=r).cpu().numpy()
+    ys, xs = np.divmod(np.arange(h * w), w)
+    ref = ((np.minimum(h - 1, ys + r) - np.maximum(0, ys - r) + 1) *
+           (np.minimum(w - 1, xs + r) - np.maximum(0, xs - r) + 1)).astype(float)
+    assert np.allclose(got, ref, rtol=2e-5, atol=0)
+
+
+def test_window_kl_slab_consistency(cuda):
+    h, w, r = 100, 300, 11
+    cfg = configs.get("c5").scaled(h, w)
+    z = wishart.generate(cfg, device=cuda)
+    full = P.window_kl(z, h, w, radius=r)
+    for r0, r1 in ((0, 33), (33, 100)):
+        s0, s1 = max(0, r0 - r), min(h, r1 + r)
+        slab = wishart.generate(cfg, s0, s1, device=cuda)
+        part = P.window_kl(slab, s1 - s0, w, radius=r, row_begin=r0 - s0, row_end=r1 - s0)
+        assert torch.equal(part, full[r0 * w:r1 * w])

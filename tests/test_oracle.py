@@ -363,3 +363,46 @@ def test_nlm_brute_force_tiny():
                 den += wq
         np.testing.assert_allclose(zhat[:, p], num / den, rtol=1e-11, atol=1e-12)
         assert W[p] == pytest.approx(den, rel=1e-12)
+
+
+# ------------------------------------------------------------- KL window oracle
+
+def test_kl_distance_properties():
+    z = rand_kappa(100, 50, 1e3)
+    for p in range(0, 100, 2):
+        zi, zj = z[:, p], z[:, p + 1]
+        # d_ii = 0 up to the long-double inverse error (~ kappa^2 2^-64, kappa <= 1e3)
+        assert abs(oracle.kl_distance(zi, zi, 4.0)) <= 1e-12
+        d = oracle.kl_distance(zi, zj, 4.0)
+        assert d >= 0  # KL divergence
+        assert d == pytest.approx(oracle.kl_distance(zj, zi, 4.0), rel=1e-15)
+        # LAPACK special case
+        fi, fj = oracle.to_full(zi[:, None])[0], oracle.to_full(zj[:, None])[0]
+        ref = 4.0 * ((np.trace(np.linalg.inv(fi) @ fj) + np.trace(np.linalg.inv(fj) @ fi)).real / 2 - 3)
+        assert d == pytest.approx(ref, rel=1e-9, abs=1e-12)
+        # invariant under congruence Z -> A Z A^H (KL between Wisharts is)
+        a = np.array([[2, 1j, 0], [0, 1, 0.5], [0.3, 0, 1]])
+        ci = pack((a @ fi @ np.conj(a.T))[None])[:, 0]
+        cj = pack((a @ fj @ np.conj(a.T))[None])[:, 0]
+        assert oracle.kl_distance(ci, cj, 4.0) == pytest.approx(d, rel=1e-7, abs=1e-10)
+
+
+def test_window_kl_constant_and_two_class():
+    h, w, r = 6, 10, 2
+    za, zb = rand_hpd(2, 51)[:, 0], rand_hpd(2, 51)[:, 1]
+    zc = np.repeat(za[:, None], h * w, axis=1)
+    got = oracle.window_kl(zc, h, w, r, 4.0, 1.0)
+    ref = np.array([clipped_count(p // w, p % w, h, w, r) for p in range(h * w)], float)
+    np.testing.assert_allclose(got, ref, rtol=1e-15)
+    xs = np.arange(h * w) % w
+    z = np.where(xs[None, :] < 5, za[:, None], zb[:, None])
+    got = oracle.window_kl(z, h, w, r, 4.0, 1.0)
+    fa, fb = oracle.to_full(za[:, None])[0], oracle.to_full(zb[:, None])[0]
+    dab = 4.0 * ((np.trace(np.linalg.inv(fa) @ fb) + np.trace(np.linalg.inv(fb) @ fa)).real / 2 - 3)
+    for p in range(h * w):
+        y, x = divmod(p, w)
+        ys = range(max(0, y - r), min(h, y + r + 1))
+        xr = range(max(0, x - r), min(w, x + r + 1))
+        same = sum(1 for _ in ys for xx in xr if (xx < 5) == (x < 5))
+        other = len(ys) * len(xr) - same
+        assert got[p] == pytest.approx(same + other * math.exp(-dab), rel=1e-12)
