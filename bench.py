@@ -391,6 +391,22 @@ def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
             gbs = n * bpm / t / 1e9
             res[f"{algo}{'_plain' if plain else ''}"] = {
                 "matrices_per_s": n / t, "ms": t * 1e3, "GB/s": gbs, "frac_hbm": gbs / peak}
+    # K1 on BASELINE configs[3] (c4: 4e8 px fp64 storage, error-free Alg. 2),
+    # 161 B / matrix
+    c4 = configs.get("c4")
+    with torch.cuda.stream(stream):
+        z4 = wishart.generate(c4, device=dev)
+        o4 = torch.empty((11, c4.n), dtype=z4.dtype, device=dev)
+        s4 = torch.empty(c4.n, dtype=torch.uint8, device=dev)
+    stream.synchronize()
+    for algo, fn in (("adjugate", P.polsar_inv_det), ("cholesky", P.polsar_inv_det_cholesky)):
+        t = _time_kernel(torch, stream, lambda: fn(z4, o4, s4, stream=stream), max(3, steps // 2))
+        gbs = c4.n * 161 / t / 1e9
+        res[f"c4_{algo}"] = {"matrices_per_s": c4.n / t, "ms": t * 1e3, "GB/s": gbs,
+                             "frac_hbm": gbs / peak, "mode": "fp64 storage" +
+                             (", error-free Alg. 2" if algo == "adjugate" else "")}
+    del z4, o4, s4
+    torch.cuda.empty_cache()
     # K3: BASELINE configs[4] window sum on one GPU
     c5 = configs.get("c5")
     with torch.cuda.stream(stream):

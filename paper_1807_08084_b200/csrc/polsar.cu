@@ -162,10 +162,24 @@ __device__ __forceinline__ dd dot3(double x1, double y1, double x2, double y2, d
     return r;
 }
 
-// Alg. 2 with every cofactor carried as hi + lo and the step-2 determinant
-// summed with Dot2 over (x_k, hi_k) plus the x_k lo_k terms: det and every
-// inverse entry come out within a few ulp, independent of the cancellation
-// (the plain form loses ~kappa^2 u for matrices with one dominant eigenvalue).
+// x1 y1 + x2 y2 + x3 y3 rounded to ~2u of the exact value (no low part):
+// exact products of the first two terms, an exact sum of their high parts,
+// the third product fused exactly into one rounding, then the corrections.
+__device__ __forceinline__ double dot3_hi(double x1, double y1, double x2, double y2, double x3,
+                                          double y3) {
+    double p1 = __dmul_rn(x1, y1), e1 = __fma_rn(x1, y1, -p1);
+    double p2 = __dmul_rn(x2, y2), e2 = __fma_rn(x2, y2, -p2);
+    double s, t;
+    two_sum(p1, p2, s, t);
+    double r = __fma_rn(x3, y3, s);
+    return __dadd_rn(r, __dadd_rn(__dadd_rn(e1, e2), t));
+}
+
+// Alg. 2 with the five cofactors that enter Eq. 6 carried as hi + lo, the
+// other four to ~2u (dot3_hi), and the step-2 determinant summed with Dot2
+// over (x_k, hi_k) plus the x_k lo_k terms: det and every inverse entry come
+// out within a few ulp, independent of the cancellation (the plain form loses
+// ~kappa^2 u for matrices with one dominant eigenvalue).
 __device__ __forceinline__ void alg2_accurate(const H9<double>& m, double* o, double& det,
                                               double& t) {
     // step 1 (Eq. 3), each cofactor as a 3-term dot product
@@ -174,10 +188,11 @@ __device__ __forceinline__ void alg2_accurate(const H9<double>& m, double* o, do
     dd bii = dot3(m.ci, m.er, -m.cr, m.ei, -m.bi, m.f);
     dd cir = dot3(m.br, m.er, -m.bi, m.ei, -m.cr, m.d);
     dd cii = dot3(m.br, m.ei, m.bi, m.er, -m.ci, m.d);
-    dd di = dot3(m.a, m.f, -m.cr, m.cr, -m.ci, m.ci);
-    dd eir = dot3(m.cr, m.br, m.ci, m.bi, -m.a, m.er);
-    dd eii = dot3(m.ci, m.br, -m.cr, m.bi, -m.a, m.ei);
-    dd fi = dot3(m.a, m.d, -m.br, m.br, -m.bi, m.bi);
+    // d_c, e_c, f_c do not enter the determinant: the high part suffices
+    const double di = dot3_hi(-m.cr, m.cr, -m.ci, m.ci, m.a, m.f);
+    const double eir = dot3_hi(m.cr, m.br, m.ci, m.bi, -m.a, m.er);
+    const double eii = dot3_hi(m.ci, m.br, -m.cr, m.bi, -m.a, m.ei);
+    const double fi = dot3_hi(-m.br, m.br, -m.bi, m.bi, m.a, m.d);
     // step 2 (Eq. 6): det = sum_k x_k (hi_k + lo_k), compensated
     double p0 = __dmul_rn(m.a, ai.hi), q0 = __fma_rn(m.a, ai.hi, -p0);
     double p1 = __dmul_rn(m.br, bir.hi), q1 = __fma_rn(m.br, bir.hi, -p1);
@@ -205,10 +220,10 @@ __device__ __forceinline__ void alg2_accurate(const H9<double>& m, double* o, do
     o[2] = __dmul_rn(t, bii.hi);
     o[3] = __dmul_rn(t, cir.hi);
     o[4] = __dmul_rn(t, cii.hi);
-    o[5] = __dmul_rn(t, di.hi);
-    o[6] = __dmul_rn(t, eir.hi);
-    o[7] = __dmul_rn(t, eii.hi);
-    o[8] = __dmul_rn(t, fi.hi);
+    o[5] = __dmul_rn(t, di);
+    o[6] = __dmul_rn(t, eir);
+    o[7] = __dmul_rn(t, eii);
+    o[8] = __dmul_rn(t, fi);
 }
 
 // ===================================================== Alg. 1 (Cholesky)
