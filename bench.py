@@ -331,9 +331,30 @@ def run_ours(args):
     return 0
 
 
-def measure_e2e(args, P, torch, dist, world, z, n, tdt, esz, dev, cfg):
+def e2e_pixels(n, esz, world):
+    """Pixels per rank for the host-buffer leg: the whole shard unless the
+    pinned host buffers of all local ranks would exceed ~60 % of host RAM
+    (an 8-GPU box pins 8 shards at once); the line reports the size used."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 64 << 30
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    per_px = 20 * esz + 1
+    cap = int(0.6 * avail / max(1, local) / per_px)
+    m = min(n, max(cap, 1 << 20))
+    return (m // 64) * 64 if m >= 64 else m
+
+
+def measure_e2e(args, P, torch, dist, world, z, n_full, tdt, esz, dev, cfg):
+    n = e2e_pixels(n_full, esz, world)
+    if world > 1:  # every rank must move the same amount
+        t = torch.tensor([n], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        n = int(t.item())
     zh = torch.empty((9, n), dtype=tdt).pin_memory()
-    zh.copy_(z)
+    zh.copy_(z[:, :n])
     oh = torch.empty((11, n), dtype=tdt).pin_memory()
     sh = torch.empty(n, dtype=torch.uint8).pin_memory()
     ws = torch.empty(3 << 30, dtype=torch.uint8, device=dev)
@@ -358,9 +379,9 @@ def measure_e2e(args, P, torch, dist, world, z, n, tdt, esz, dev, cfg):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
     del ws
-    return {"value": n * world / t, "unit": UNIT, "h2d_bytes_per_step": 9 * n * esz,
-            "d2h_bytes_per_step": 11 * n * esz + n, "steps": args.e2e_steps,
-            "ms_per_step": t * 1e3,
+    return {"value": n * world / t, "unit": UNIT, "h2d_bytes_per_step": 9 * n * esz * world,
+            "d2h_bytes_per_step": (11 * n * esz + n) * world, "steps": args.e2e_steps,
+            "ms_per_step": t * 1e3, "pixels_per_gpu": n,
             "path": "polsar_inv_det_host: pinned host -> 3-slot chunked H2D/kernel/D2H pipeline"}
 
 
