@@ -1,0 +1,94 @@
+// common.cuh -- part of libpolsar.so (B200, sm_100a); arXiv 1807.08084.
+// Layout, ownership and error conventions: include/polsar.h.  Design notes:
+// DESIGN.md.  Nothing here is shared with oracle/.
+//
+// Shared device helpers: round-to-nearest arithmetic overloads, streaming
+// 16-byte I/O, the packed Hermitian type, launch-geometry and error helpers.
+//
+// Bit-stability: every floating-point operation of the per-matrix device
+// functions is an explicit round-to-nearest intrinsic (__fma_rn, __dmul_rn,
+// __dadd_rn, ...), so ptxas cannot contract or reassociate differently in the
+// vector body and the scalar tail: both yield identical bits.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "../../include/polsar.h"
+
+namespace polsar_impl {
+
+// ------------------------------------------------------------------ errors
+// (defined in abi.cu; thread-local, read back by polsar_last_error)
+int fail(int code, const char* msg);
+int launch_check(const char* what);
+
+// --------------------------------------------------------- launch geometry
+int num_sms();
+// one thread per work item, the whole batch in one grid (capped at 2^31-1
+// CTAs; the kernels' grid-stride loops take any remainder)
+int grid_full(int64_t work, int threads);
+// enough CTAs for every SM to hold its resident maximum several times over
+int grid_for(int64_t work, int threads);
+
+// ----------------------------------------------------- rounding intrinsics
+// Overloads so one template body serves fp32 and fp64 arithmetic.
+__device__ __forceinline__ double MUL(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float MUL(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double ADD(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float ADD(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double SUB(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float SUB(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double FMA(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float FMA(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double RCP(double a) { return __drcp_rn(a); }
+__device__ __forceinline__ float RCP(float a) { return __frcp_rn(a); }
+__device__ __forceinline__ double SQRT(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ float SQRT(float a) { return __fsqrt_rn(a); }
+
+// ------------------------------------------------------ streaming HBM I/O
+// Plain 16-byte global loads and stores (LDG.E.128 / STG.E.128).  Measured
+// on B200 at c3 size (tools/micro/k1_tune.cu): the default cache policy beats
+// ld.global.nc.L1::no_allocate + st.global.cs by ~5 % for this 9-in / 11-out
+// stream, reaching 103 % of the driver's copy peak with one 16-B vector per
+// plane per thread and 128-thread CTAs over the whole batch.
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return *p; }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return *p; }
+__device__ __forceinline__ float ld_stream(const float* p) { return *p; }
+__device__ __forceinline__ double ld_stream(const double* p) { return *p; }
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { *p = v; }
+__device__ __forceinline__ void st_stream(double2* p, double2 v) { *p = v; }
+__device__ __forceinline__ void st_stream(float* p, float v) { *p = v; }
+__device__ __forceinline__ void st_stream(double* p, double v) { *p = v; }
+
+// ------------------------------------------------------------ matrix types
+template <typename T>
+struct H9 {  // packed Hermitian
+    T a, br, bi, cr, ci, d, er, ei, f;
+};
+
+template <typename T>
+struct R11 {  // 9 inverse components, det, det^-1, status
+    T v[11];
+    uint8_t status;
+};
+
+// tau * a*d*f, tau = 16 u_in (R-5)
+template <typename S>
+struct Tau;
+template <>
+struct Tau<float> {
+    static constexpr double v = 16.0 * 5.9604644775390625e-08;  // 16 * 2^-24
+};
+template <>
+struct Tau<double> {
+    static constexpr double v = 16.0 * 1.1102230246251565e-16;  // 16 * 2^-53
+};
+
+template <typename T>
+__device__ __forceinline__ bool finite_pos(T x) {
+    return x > T(0) && x < T(INFINITY);
+}
+
+}  // namespace polsar_impl
