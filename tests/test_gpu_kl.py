@@ -50,3 +50,14 @@ def test_window_kl_slab_consistency(cuda):
         slab = wishart.generate(cfg, s0, s1, device=cuda)
         part = P.window_kl(slab, s1 - s0, w, radius=r, row_begin=r0 - s0, row_end=r1 - s0)
         assert torch.equal(part, full[r0 * w:r1 * w])
+
+
+def test_window_kl_c5_full_size_sampled(cuda):
+    cfg = configs.get("c5")
+    h, w = cfg.height, cfg.width
+    z = wishart.generate(cfg, device=cuda)
+    got = P.window_kl(z, h, w, radius=cfg.radius, looks=cfg.looks, h=cfg.h).cpu().numpy()
+    rng = np.random.default_rng(6)
+    idx = np.concatenate([[0, w - 1, h * w - 1, 64 * w + 64], rng.integers(0, h * w, 2000)])
+    ref = oracle.window_kl_threaded(z.cpu().numpy(), h, w, cfg.radius, cfg.looks, cfg.h, idx, THREADS)
+    assert (np.abs(got[idx] - ref) / ref).max() <= 2e-5

@@ -60,3 +60,18 @@ def test_nlm_slab_consistency(cuda):
         part, pw = P.nlm_filter(slab, s1 - s0, w, radius=r, row_begin=r0 - s0, row_end=r1 - s0)
         assert torch.equal(part, full[:, r0 * w:r1 * w])
         assert torch.equal(pw, fw[r0 * w:r1 * w])
+
+
+def test_nlm_c5_full_size_sampled(cuda):
+    cfg = configs.get("c5")
+    h, w = cfg.height, cfg.width
+    z = wishart.generate(cfg, device=cuda)
+    zhat, W = P.nlm_filter(z, h, w, radius=cfg.radius, looks=cfg.looks, h=cfg.h)
+    rng = np.random.default_rng(5)
+    idx = np.concatenate([[0, w - 1, h * w - 1, 64 * w + 64], rng.integers(0, h * w, 2000)])
+    rz, rw = oracle.nlm_threaded(z.cpu().numpy(), h, w, cfg.radius, cfg.looks, cfg.h, idx, THREADS)
+    ii = torch.as_tensor(idx, device=cuda)
+    got = zhat[:, ii].cpu().numpy().astype(np.float64)
+    err = np.max(np.abs(got - rz), axis=0) / np.max(np.abs(rz), axis=0)
+    assert err.max() <= 2e-5
+    assert (np.abs(W[ii].cpu().numpy() - rw) / rw).max() <= 2e-5
