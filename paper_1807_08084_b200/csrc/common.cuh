@@ -68,12 +68,6 @@ struct H9 {  // packed Hermitian
     T a, br, bi, cr, ci, d, er, ei, f;
 };
 
-template <typename T>
-struct R11 {  // 9 inverse components, det, det^-1, status
-    T v[11];
-    uint8_t status;
-};
-
 // tau * a*d*f, tau = 16 u_in (R-5)
 template <typename S>
 struct Tau;
