@@ -17,6 +17,18 @@
 
 #include "../../include/polsar.h"
 
+// Bounds checks for debug builds (-DPOLSAR_DEBUG_BOUNDS, tools/debug_build.sh):
+// device-side asserts on shared-memory and global indexing.  Compiled out of
+// the product library.
+#ifdef POLSAR_DEBUG_BOUNDS
+#include <assert.h>
+#define POLSAR_CHECK(c) assert(c)
+#else
+#define POLSAR_CHECK(c) \
+    do {                \
+    } while (0)
+#endif
+
 namespace polsar_impl {
 
 // ------------------------------------------------------------------ errors

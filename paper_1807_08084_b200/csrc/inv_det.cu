@@ -54,6 +54,7 @@ k_inv_det_vec(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict_
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_groups;
          g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = g * W;
+        POLSAR_CHECK(p + W <= n_groups * W && p % W == 0);
         S in[9][W];
 #pragma unroll
         for (int k = 0; k < 9; ++k) unpack<V, S>(ld_stream(reinterpret_cast<const V*>(z + k * ld + p)), in[k]);

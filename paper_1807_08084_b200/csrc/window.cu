@@ -163,6 +163,7 @@ k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
 #pragma unroll 2
                 for (int wx = -R; wx <= R; ++wx) {
                     T zj[9];
+                    POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
 #pragma unroll
                     for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
                     const WT gj = rowg[wx];
@@ -172,6 +173,7 @@ k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
             } else {
                 for (int wx = -R; wx <= R; ++wx) {
                     T zj[9];
+                    POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
 #pragma unroll
                     for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
                     const WT gj = rowg[wx];
@@ -187,6 +189,7 @@ k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
             // one of the RB-1 rows at either end: only some owned pixels reach it
             for (int wx = -R; wx <= R; ++wx) {
                 T zj[9];
+                POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
 #pragma unroll
                 for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
                 const WT gj = rowg[wx];
@@ -319,6 +322,7 @@ k_nlm_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
         for (int r = 0; r < RB; ++r) rok[r] = (wy - r >= -R) && (wy - r <= R);  // warp-uniform
         for (int wx = -R; wx <= R; ++wx) {
             T zj[9];
+            POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
 #pragma unroll
             for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
             const WT gj = rowg[wx];
@@ -614,6 +618,7 @@ k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows,
             const double* srow = ws + pl * P + (rok ? gy : 0) * width;
             double* drow = dst + pl * CHP + row * SW;
             for (int col = lane; col < SW; col += 32) {
+                POLSAR_CHECK(pl * CHP + row * SW + col < V3_NP * CHP);
                 const int64_t gxx = x0 - XOFF + col;
                 const bool ok = rok && gxx >= 0 && gxx < width;
                 cp_async8(drow + col, srow + (ok ? gxx : 0), ok);
@@ -678,6 +683,7 @@ k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows,
 #pragma unroll 1
                 for (int wx = -R; wx <= R; ++wx) {
                     double zj[9], uj[9];
+                    POLSAR_CHECK(row * SW + XOFF + tx + wx >= 0 && row * SW + XOFF + tx + wx < CHP);
 #pragma unroll
                     for (int k = 0; k < 9; ++k) {
                         zj[k] = rb[k * CHP + wx];
@@ -706,6 +712,7 @@ k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows,
 #pragma unroll 1
                 for (int wx = -R; wx <= R; ++wx) {
                     double zj[9], uj[9];
+                    POLSAR_CHECK(row * SW + XOFF + tx + wx >= 0 && row * SW + XOFF + tx + wx < CHP);
 #pragma unroll
                     for (int k = 0; k < 9; ++k) {
                         zj[k] = rb[k * CHP + wx];
