@@ -66,10 +66,12 @@ __device__ __forceinline__ float SQRT(float a) { return __fsqrt_rn(a); }
 // stream, reaching 103 % of the driver's copy peak with one 16-B vector per
 // plane per thread and 128-thread CTAs over the whole batch.
 __device__ __forceinline__ float4 ld_stream(const float4* p) { return *p; }
+__device__ __forceinline__ float2 ld_stream(const float2* p) { return *p; }
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return *p; }
 __device__ __forceinline__ float ld_stream(const float* p) { return *p; }
 __device__ __forceinline__ double ld_stream(const double* p) { return *p; }
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { *p = v; }
+__device__ __forceinline__ void st_stream(float2* p, float2 v) { *p = v; }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { *p = v; }
 __device__ __forceinline__ void st_stream(float* p, float v) { *p = v; }
 __device__ __forceinline__ void st_stream(double* p, double v) { *p = v; }

@@ -28,8 +28,37 @@ struct Vec<double> {
     static constexpr int n = 2;
 };
 
+#ifndef K2_VEC
+#define K2_VEC Vec2f
+#endif
+// Alg. 1 (K2) takes 2 fp32 pixels per thread instead of 4: its DSQRT / DRCP
+// sequences are latency-bound, and twice the threads hide more of it
+// (measured on B200).
+struct Vec2f {
+    typedef float2 type;
+    static constexpr int n = 2;
+};
+struct Vec1f {
+    typedef float type;
+    static constexpr int n = 1;
+};
+template <typename S, int ALGO>
+struct VecSel {
+    typedef Vec<S> V;
+};
+template <>
+struct VecSel<float, 1> {
+    typedef K2_VEC V;
+};
+
 template <typename V, typename S>
 __device__ __forceinline__ void unpack(const V& v, S* x);
+template <>
+__device__ __forceinline__ void unpack<float2, float>(const float2& v, float* x) {
+    x[0] = v.x; x[1] = v.y;
+}
+template <>
+__device__ __forceinline__ void unpack<float, float>(const float& v, float* x) { x[0] = v; }
 template <>
 __device__ __forceinline__ void unpack<float4, float>(const float4& v, float* x) {
     x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
@@ -42,6 +71,8 @@ __device__ __forceinline__ float4 pack4(const float* x) { return make_float4(x[0
 __device__ __forceinline__ double2 pack2(const double* x) { return make_double2(x[0], x[1]); }
 __device__ __forceinline__ float4 packv(const float* x, float4*) { return pack4(x); }
 __device__ __forceinline__ double2 packv(const double* x, double2*) { return pack2(x); }
+__device__ __forceinline__ float2 packv(const float* x, float2*) { return make_float2(x[0], x[1]); }
+__device__ __forceinline__ float packv(const float* x, float*) { return x[0]; }
 
 constexpr int K1_THREADS = 128;
 
@@ -49,8 +80,9 @@ template <typename S, int ALGO, int MATH>
 __global__ void __launch_bounds__(K1_THREADS)
 k_inv_det_vec(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
               int64_t n_groups, int64_t ld) {
-    typedef typename Vec<S>::type V;
-    constexpr int W = Vec<S>::n;
+    typedef typename VecSel<S, ALGO>::V VV;
+    typedef typename VV::type V;
+    constexpr int W = VV::n;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_groups;
          g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = g * W;
@@ -73,13 +105,15 @@ k_inv_det_vec(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict_
         for (int k = 0; k < 11; ++k)
             st_stream(reinterpret_cast<V*>(out + k * ld + p), packv(res[k], (V*)nullptr));
         if (status) {
-            if (W == 4) {
-                uint32_t w = (uint32_t)st[0] | ((uint32_t)st[1 % W] << 8) |
-                             ((uint32_t)st[2 % W] << 16) | ((uint32_t)st[3 % W] << 24);
+            if constexpr (W == 4) {
+                uint32_t w = (uint32_t)st[0] | ((uint32_t)st[1] << 8) | ((uint32_t)st[2] << 16) |
+                             ((uint32_t)st[3] << 24);
                 *reinterpret_cast<uint32_t*>(status + p) = w;
-            } else {
-                uint16_t w = (uint16_t)(st[0] | (st[1 % W] << 8));
+            } else if constexpr (W == 2) {
+                uint16_t w = (uint16_t)(st[0] | (st[1] << 8));
                 *reinterpret_cast<uint16_t*>(status + p) = w;
+            } else {
+                status[p] = st[0];
             }
         }
     }
@@ -109,7 +143,7 @@ int launch_inv_det(const void* zv, void* outv, uint8_t* status, int64_t n, int64
                    cudaStream_t s) {
     const S* z = (const S*)zv;
     S* out = (S*)outv;
-    constexpr int W = Vec<S>::n;
+    constexpr int W = VecSel<S, ALGO>::V::n;
     bool aligned = ((uintptr_t)z % 16 == 0) && ((uintptr_t)out % 16 == 0) && (ld % W == 0) &&
                    (status == nullptr || (uintptr_t)status % W == 0);
     int64_t n_vec = aligned ? (n / W) * W : 0;
