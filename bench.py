@@ -442,7 +442,7 @@ def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
     with torch.cuda.stream(stream):
         z5 = wishart.generate(c5, device=dev)
         code = P.dtype_code(z5.dtype)
-        ws = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, code),
+        ws = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, c5.radius, code),
                          dtype=torch.uint8, device=dev)
         w5 = torch.empty(c5.n, dtype=z5.dtype, device=dev)
     stream.synchronize()
@@ -542,7 +542,7 @@ def run_window(args):
             own = wishart.generate(cfg, r0, r1, device=dev, table=tab, height=H)
             slab[:, ob * W:oe * W] = own
         code = P.dtype_code(slab.dtype)
-        ws = torch.empty(P.polsar_window_workspace_bytes(s1 - s0, W, code), dtype=torch.uint8, device=dev)
+        ws = torch.empty(P.polsar_window_workspace_bytes(s1 - s0, W, R, code), dtype=torch.uint8, device=dev)
         out = torch.empty((oe - ob) * W, dtype=slab.dtype, device=dev)
         outz = torch.empty((9, (oe - ob) * W), dtype=slab.dtype, device=dev)
     stream.synchronize()

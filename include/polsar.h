@@ -105,9 +105,12 @@ int polsar_inv_det_cholesky(const void* z, void* out, uint8_t* status, int64_t n
 int polsar_inv_det_blocks(const void* z, void* out, uint8_t* status, int64_t n, int64_t ld,
                           int nblocks, int dtype, void* cuda_stream);
 
-/* polsar_window_workspace_bytes -- bytes of device workspace
- * polsar_window_distance needs for a slab of slab_rows x width pixels. */
-size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int dtype);
+/* polsar_window_workspace_bytes -- bytes of device workspace the window
+ * entry points (polsar_window_distance, polsar_nlm_filter, polsar_window_kl)
+ * need for a slab of slab_rows x width pixels at this radius and dtype.
+ * (The default symmetric window kernel stores the 2R(R+1) forward pair
+ * weights of every pixel: ~1.07 KB per pixel at R = 11, fp32 weights.) */
+size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radius, int dtype);
 
 /* polsar_window_distance -- non-local-means search-window sum (the workload
  * of PAPER.md:77-80 [§I]; formula of BASELINE.json configs[4]):
@@ -122,7 +125,7 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int dtype
  *               <= slab_rows); out receives (e - b) x width values, row-major.
  *   radius R (>= 0, <= 16; the paper's 23x23 window is R = 11), looks L (> 0),
  *               h (> 0).
- *   workspace : device, polsar_window_workspace_bytes(slab_rows, width, dtype)
+ *   workspace : device, polsar_window_workspace_bytes(slab_rows, width, radius, dtype)
  *   dtype     : POLSAR_F32 (fp32 storage, fp64 pair determinant, fp32
  *               weight) or POLSAR_F64 (fp64 throughout), or the _PLAIN
  *               variants (storage precision throughout). */
@@ -151,7 +154,7 @@ int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows
  *   out_w  : device, (e - b) x width values of W, or NULL
  *   out_z  : device, 9 planes of (e - b) x width filtered pixels (packed
  *            field order), plane stride ld_out >= (e - b) * width.
- * Workspace: polsar_window_workspace_bytes(slab_rows, width, dtype). */
+ * Workspace: polsar_window_workspace_bytes(slab_rows, width, radius, dtype). */
 int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
                       int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
                       double h, void* workspace, void* out_w, void* out_z, int64_t ld_out,

@@ -124,8 +124,8 @@ def inv_det(z, algo: str = "adjugate", plain: bool = False, with_status: bool = 
     return (out, status) if with_status else out
 
 
-def polsar_window_workspace_bytes(slab_rows: int, width: int, dtype: int) -> int:
-    return int(lib().polsar_window_workspace_bytes(slab_rows, width, dtype))
+def polsar_window_workspace_bytes(slab_rows: int, width: int, radius: int, dtype: int) -> int:
+    return int(lib().polsar_window_workspace_bytes(slab_rows, width, radius, dtype))
 
 
 def polsar_window_distance(z, width, slab_rows, out_row_begin, out_row_end, radius, looks, h,
@@ -135,7 +135,7 @@ def polsar_window_distance(z, width, slab_rows, out_row_begin, out_row_end, radi
     _dev_check(z, workspace, out)
     ld = _planes(z, 9)
     code = dtype_code(z.dtype, plain)
-    need = polsar_window_workspace_bytes(slab_rows, width, code)
+    need = polsar_window_workspace_bytes(slab_rows, width, radius, code)
     if workspace.numel() * workspace.element_size() < need:
         raise ValueError(f"workspace needs {need} bytes")
     if out.numel() < (out_row_end - out_row_begin) * width or out.dtype != z.dtype:
@@ -153,7 +153,7 @@ def window_distance(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, 
     torch = _torch()
     row_end = height if row_end is None else row_end
     code = dtype_code(z.dtype, plain)
-    ws = torch.empty(polsar_window_workspace_bytes(height, width, code), dtype=torch.uint8,
+    ws = torch.empty(polsar_window_workspace_bytes(height, width, radius, code), dtype=torch.uint8,
                      device=z.device)
     out = torch.empty((row_end - row_begin) * width, dtype=z.dtype, device=z.device)
     return polsar_window_distance(z, width, height, row_begin, row_end, radius, looks, h, ws, out,
@@ -166,7 +166,7 @@ def polsar_window_kl(z, width, slab_rows, out_row_begin, out_row_end, radius, lo
     _dev_check(z, workspace, out)
     ld = _planes(z, 9)
     code = dtype_code(z.dtype)
-    need = polsar_window_workspace_bytes(slab_rows, width, code)
+    need = polsar_window_workspace_bytes(slab_rows, width, radius, code)
     if workspace.numel() * workspace.element_size() < need:
         raise ValueError(f"workspace needs {need} bytes")
     if out.numel() < (out_row_end - out_row_begin) * width or out.dtype != z.dtype:
@@ -183,7 +183,7 @@ def window_kl(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, row_en
     torch = _torch()
     row_end = height if row_end is None else row_end
     code = dtype_code(z.dtype)
-    ws = torch.empty(polsar_window_workspace_bytes(height, width, code), dtype=torch.uint8,
+    ws = torch.empty(polsar_window_workspace_bytes(height, width, radius, code), dtype=torch.uint8,
                      device=z.device)
     out = torch.empty((row_end - row_begin) * width, dtype=z.dtype, device=z.device)
     return polsar_window_kl(z, width, height, row_begin, row_end, radius, looks, h, ws, out,
@@ -198,7 +198,7 @@ def polsar_nlm_filter(z, width, slab_rows, out_row_begin, out_row_end, radius, l
     ld = _planes(z, 9)
     ld_out = _planes(out_z, 9)
     code = dtype_code(z.dtype, plain)
-    need = polsar_window_workspace_bytes(slab_rows, width, code)
+    need = polsar_window_workspace_bytes(slab_rows, width, radius, code)
     if workspace.numel() * workspace.element_size() < need:
         raise ValueError(f"workspace needs {need} bytes")
     if out_z.dtype != z.dtype or (out_w is not None and out_w.dtype != z.dtype):
@@ -217,7 +217,7 @@ def nlm_filter(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, row_e
     row_end = height if row_end is None else row_end
     m = (row_end - row_begin) * width
     code = dtype_code(z.dtype, plain)
-    ws = torch.empty(polsar_window_workspace_bytes(height, width, code), dtype=torch.uint8,
+    ws = torch.empty(polsar_window_workspace_bytes(height, width, radius, code), dtype=torch.uint8,
                      device=z.device)
     out_z = torch.empty((9, m), dtype=z.dtype, device=z.device)
     out_w = torch.empty(m, dtype=z.dtype, device=z.device)

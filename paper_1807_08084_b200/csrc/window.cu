@@ -7,6 +7,8 @@
 //   K6  polsar_window_kl         window sum with the symmetric Wishart KL distance
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "alg.cuh"
 
 namespace polsar_impl {
@@ -778,17 +780,248 @@ int launch_window_kl(const void* zv, int64_t ld, int64_t width, int64_t slab_row
     return launch_check("polsar_window_kl: launch failed");
 }
 
-// Window kernel variant for the fp64-determinant modes: 2 (direct Eq. 6 on
-// S = Z_i + Z_j, default: fastest measured on B200) or 3 (cubic expansion
-// over per-pixel adjugates, fewer FP64 ops but smem/register bound);
-// POLSAR_WINDOW_VARIANT=3 selects the latter (A/B runs; both are parity-tested).
+// Window kernel variant (R <= 12): 4 (symmetric two-pass, default), 2 (direct
+// Eq. 6 on S = Z_i + Z_j for every ordered pair), 3 (cubic expansion over
+// per-pixel adjugates).  POLSAR_WINDOW_VARIANT=2|3 selects the alternatives
+// for A/B runs; all are parity-tested.  R > 12 always runs variant 2.
 int window_variant() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("POLSAR_WINDOW_VARIANT");
-        v = (e && e[0] == '3') ? 3 : 2;
+        v = (e && (e[0] == '2' || e[0] == '3')) ? e[0] - '0' : 4;
     }
     return v;
+}
+
+// ------------------------------------------------------------------------
+// K3 (symmetric, default for R <= V3_RMAX): d_ij = d_ji (the window is
+// symmetric and det((Z_i+Z_j)/2) is), so each unordered pair is evaluated
+// once.  Pass 1 (k_window_fwd) computes, for every pixel i, the weights of its
+// 2R(R+1) "forward" neighbours j = i + delta (delta_y > 0, or delta_y = 0 and
+// delta_x > 0): their sum F_i, and each weight stored at wbuf[delta][i].
+// Pass 2 (k_window_bwd) adds, for every output pixel j, the stored weights of
+// its backward neighbours: W_j = 1 + F_j + sum_delta wbuf[delta][j - delta]
+// (d_jj = 0 contributes exactly 1).  Half the FP64 work of k_window_sum for
+// 1068 B/pixel of workspace traffic (fp32 weights, R = 11); every sum is in a
+// fixed order, so results are bit-reproducible and slab decompositions are
+// exact.
+__host__ __device__ __forceinline__ int fwd_count(int R) { return 2 * R * (R + 1); }
+__device__ __forceinline__ int fwd_index(int dy, int dx, int R) {
+    return dy == 0 ? dx - 1 : R + (dy - 1) * (2 * R + 1) + (dx + R);
+}
+
+// Shared-memory halo pixel of pass 1: the 9 planes and g in one 10-slot record
+// (stride 10 T: 16-byte aligned for T = double, 8-byte for float), read with
+// five 2-wide loads from one address.  Record strides of 5 (double2) / 5
+// (float2) bank units are odd, so a warp's loads are conflict-free.
+template <typename T>
+struct Vec2Of;
+template <>
+struct Vec2Of<double> { using type = double2; };
+template <>
+struct Vec2Of<float> { using type = float2; };
+
+// g (WT) carried in the record's T slot, bit-exact.
+template <typename T, typename WT>
+__device__ __forceinline__ T pack_g(WT v) {
+    if constexpr (sizeof(T) == sizeof(WT)) return (T)v;
+    else return __longlong_as_double((long long)__float_as_uint(v));
+}
+template <typename T, typename WT>
+__device__ __forceinline__ WT unpack_g(T v) {
+    if constexpr (sizeof(T) == sizeof(WT)) return (WT)v;
+    else return __uint_as_float((unsigned)__double_as_longlong(v));
+}
+
+template <typename T, typename WT>
+__device__ __forceinline__ void load_rec(const T* rec, T (&zj)[9], WT& gj) {
+    using V = typename Vec2Of<T>::type;
+    const V* p = reinterpret_cast<const V*>(rec);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const V v = p[k];
+        zj[2 * k] = v.x;
+        zj[2 * k + 1] = v.y;
+    }
+    const V v = p[4];
+    zj[8] = v.x;
+    gj = unpack_g<T, WT>(v.y);
+}
+
+template <typename S, typename T, typename WT, int TY, int RB>
+__global__ void __launch_bounds__(K3_TX * TY / RB, 1)
+k_window_fwd(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
+             int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
+             int alpha_is_2, WT* __restrict__ wbuf, double* __restrict__ fbuf) {
+    static_assert(sizeof(WT) <= sizeof(T), "g must fit a T slot");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int HW = K3_TX + 2 * R;   // halo columns x0-R .. x0+TX-1+R
+    const int HH = TY + R;          // halo rows y0 .. y0+TY-1+R (forward only)
+    const int HP = HW * HH;
+    T* sz = reinterpret_cast<T*>(smem_raw);  // HP records of 10 T
+    const int64_t N = slab_rows * width;
+
+    const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
+    const int64_t y0 = row_begin + (int64_t)blockIdx.y * TY;
+    for (int q = threadIdx.x; q < HP; q += blockDim.x) {
+        int hy = q / HW, hx = q % HW;
+        int64_t gy = y0 + hy, gx = x0 - R + hx;
+        bool in = gy < slab_rows && gx >= 0 && gx < width;
+        int64_t p = in ? gy * width + gx : 0;
+        T* rec = sz + 10 * q;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) rec[k] = in ? (T)z[k * ld + p] : T(0);
+        rec[9] = pack_g<T, WT>(in ? g[p] : WT(0));
+    }
+    __syncthreads();
+
+    const int tx = threadIdx.x % K3_TX;
+    const int ty0 = (threadIdx.x / K3_TX) * RB;
+    const int64_t gx = x0 + tx;
+    T zi[RB][9];
+    WT gi[RB];
+    double acc[RB];
+    bool own[RB];
+    int64_t pi[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        const int64_t gy = y0 + ty0 + r;
+        own[r] = gx < width && gy < row_end;
+        pi[r] = gy * width + gx;
+        load_rec(sz + 10 * ((ty0 + r) * HW + (tx + R)), zi[r], gi[r]);
+        acc[r] = 0.0;
+    }
+    const WT alpha = (WT)alpha_d;
+    const bool a2 = alpha_is_2 != 0;
+    const bool interior_x = (x0 - R >= 0) && (x0 + K3_TX + R <= width);
+
+    for (int wy = 0; wy <= R + RB - 1; ++wy) {
+        const int64_t gyj = y0 + ty0 + wy;
+        if (gyj >= slab_rows) break;  // warp-uniform
+        const int hy = ty0 + wy;
+        const T* rec = sz + 10 * (hy * HW + tx);  // neighbour wx = -R
+        WT row[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) row[r] = WT(0);
+        if (wy >= RB && wy <= R) {
+            // every owned pixel sees this row at dy = wy - r in [1, R]: full rows.
+            // wp[r] walks the weight planes delta = (wy - r, wx), consecutive in wx.
+            WT* wp[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) wp[r] = wbuf + (int64_t)fwd_index(wy - r, -R, R) * N + pi[r];
+            for (int wx = -R; wx <= R; ++wx, rec += 10) {
+                POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
+                T zj[9];
+                WT gj;
+                load_rec(rec, zj, gj);
+                const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+                    WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
+                    w = colok ? w : WT(0);
+                    row[r] += w;
+                    if (colok && own[r]) *wp[r] = w;
+                    wp[r] += N;
+                }
+            }
+        } else {
+            for (int wx = -R; wx <= R; ++wx, rec += 10) {
+                POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
+                T zj[9];
+                WT gj;
+                load_rec(rec, zj, gj);
+                const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+                    const int dy = wy - r;
+                    if (dy >= 0 && dy <= R && (dy > 0 || wx > 0)) {  // warp-uniform
+                        WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
+                        w = colok ? w : WT(0);
+                        row[r] += w;
+                        if (colok && own[r]) wbuf[(int64_t)fwd_index(dy, wx, R) * N + pi[r]] = w;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acc[r] += (double)row[r];
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+        if (gx < width && y0 + ty0 + r < row_end) fbuf[pi[r]] = acc[r];
+}
+
+// Pass 2: W_j = 1 + F_j + sum over backward neighbours, one thread per pixel.
+// Each (delta_y) row of weights is summed in WT, then added in double.
+template <typename S, typename WT>
+__global__ void __launch_bounds__(256)
+k_window_bwd(const WT* __restrict__ wbuf, const double* __restrict__ fbuf, int64_t width,
+             int64_t slab_rows, int64_t row_begin, int64_t row_end, int R, S* __restrict__ out) {
+    const int64_t N = slab_rows * width;
+    const int64_t m = (row_end - row_begin) * width;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = row_begin + q / width, x = q % width;
+        const int64_t p = y * width + x;
+        double acc = 1.0 + fbuf[p];
+        const bool inx = x - R >= 0 && x + R < width;
+        for (int dy = 0; dy <= R; ++dy) {
+            if (y - dy < 0) break;
+            const int dx0 = dy == 0 ? 1 : -R;
+            const WT* base = wbuf + (int64_t)fwd_index(dy, dx0, R) * N + p - (int64_t)dy * width - dx0;
+            WT rowp = WT(0);
+            if (inx) {
+                for (int dx = dx0; dx <= R; ++dx) rowp += base[(int64_t)(dx - dx0) * (N - 1)];
+            } else {
+                for (int dx = dx0; dx <= R; ++dx)
+                    if (x - dx >= 0 && x - dx < width) rowp += base[(int64_t)(dx - dx0) * (N - 1)];
+            }
+            acc += (double)rowp;
+        }
+        out[q] = (S)acc;
+    }
+}
+
+template <typename T, typename WT>
+size_t window_fwd_smem(int TY, int R) {
+    return (size_t)(K3_TX + 2 * R) * (TY + R) * 10 * sizeof(T);
+}
+
+// workspace: g (N x WT) | F (N x double) | wbuf (fwd_count(R) x N x WT)
+template <typename WT>
+size_t window_sym_bytes(int64_t n, int R) {
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    return up(n * sizeof(WT)) + up(n * sizeof(double)) + up((size_t)fwd_count(R) * n * sizeof(WT));
+}
+
+template <typename S, typename T, typename WT>
+int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
+                      int64_t re, int R, double looks, double h, void* wsv, void* outv,
+                      cudaStream_t s) {
+    const S* z = (const S*)zv;
+    const int64_t n = slab_rows * width;
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    unsigned char* ws = (unsigned char*)wsv;
+    WT* g = (WT*)ws;
+    double* fbuf = (double*)(ws + up(n * sizeof(WT)));
+    WT* wbuf = (WT*)(ws + up(n * sizeof(WT)) + up(n * sizeof(double)));
+    k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
+    const double alpha = looks / (2.0 * h);
+    // pass 1 covers the output rows and the R rows above them (their forward
+    // pairs are the backward pairs of the first output rows)
+    const int64_t p0 = rb - R > 0 ? rb - R : 0;
+    constexpr int TY = 32, RB = 2;
+    const size_t smem = window_fwd_smem<T, WT>(TY, R);
+    auto kern = k_window_fwd<S, T, WT, TY, RB>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
+    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - p0 + TY - 1) / TY));
+    kern<<<grid, K3_TX * TY / RB, smem, s>>>(z, ld, width, slab_rows, p0, re, R, g, alpha,
+                                             alpha == 2.0 ? 1 : 0, wbuf, fbuf);
+    k_window_bwd<S, WT><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
+        wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
+    return launch_check("polsar_window_distance: launch failed");
 }
 
 }  // namespace
@@ -798,12 +1031,18 @@ using namespace polsar_impl;
 
 extern "C" {
 
-size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int dtype) {
-    if (slab_rows < 0 || width < 0) return 0;
-    // fp64-determinant modes: 20 fp64 planes per pixel (z, weighted adj(Z),
-    // det, g); F32_PLAIN: one fp32 plane of g (rounded up to 256 bytes)
-    size_t per = (dtype == POLSAR_F32_PLAIN) ? 4 : 20 * 8;
-    return (((size_t)(slab_rows * width) * per) + 255) / 256 * 256;
+size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radius, int dtype) {
+    if (slab_rows < 0 || width < 0 || radius < 0) return 0;
+    const int64_t n = slab_rows * width;
+    const bool wt64 = dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN;
+    // the largest need of the kernels the call may run: direct form / NLM
+    // (one plane of g), the expansion form and KL (20 fp64 planes), the
+    // symmetric form (g, F and 2R(R+1) weight planes)
+    size_t b = (((size_t)n * (wt64 ? 8 : 4)) + 255) / 256 * 256;
+    if (dtype != POLSAR_F32_PLAIN) b = std::max(b, ((size_t)n * 160 + 255) / 256 * 256);
+    if (radius <= V3_RMAX)
+        b = std::max(b, wt64 ? window_sym_bytes<double>(n, radius) : window_sym_bytes<float>(n, radius));
+    return b;
 }
 
 int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
@@ -823,6 +1062,10 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
             if (radius <= V3_RMAX && window_variant() == 3)
                 return launch_window_v3<float, float>(z, ld, width, slab_rows, out_row_begin,
                                                       out_row_end, radius, looks, h, workspace, out, s);
+            if (radius <= V3_RMAX && window_variant() == 4)
+                return launch_window_sym<float, double, float>(z, ld, width, slab_rows, out_row_begin,
+                                                               out_row_end, radius, looks, h, workspace,
+                                                               out, s);
             return launch_window<float, double, float>(z, ld, width, slab_rows, out_row_begin,
                                                        out_row_end, radius, looks, h, workspace, out, s);
         case POLSAR_F64:
@@ -830,9 +1073,17 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
             if (radius <= V3_RMAX && window_variant() == 3)
                 return launch_window_v3<double, double>(z, ld, width, slab_rows, out_row_begin,
                                                         out_row_end, radius, looks, h, workspace, out, s);
+            if (radius <= V3_RMAX && window_variant() == 4)
+                return launch_window_sym<double, double, double>(z, ld, width, slab_rows, out_row_begin,
+                                                                 out_row_end, radius, looks, h,
+                                                                 workspace, out, s);
             return launch_window<double, double, double>(z, ld, width, slab_rows, out_row_begin,
                                                          out_row_end, radius, looks, h, workspace, out, s);
         case POLSAR_F32_PLAIN:
+            if (radius <= V3_RMAX && window_variant() == 4)
+                return launch_window_sym<float, float, float>(z, ld, width, slab_rows, out_row_begin,
+                                                              out_row_end, radius, looks, h, workspace,
+                                                              out, s);
             return launch_window<float, float, float>(z, ld, width, slab_rows, out_row_begin,
                                                       out_row_end, radius, looks, h, workspace, out, s);
         default: return fail(POLSAR_EINVAL, "bad dtype");

@@ -66,7 +66,7 @@ def test_loads_and_validates_without_gpu():
     assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 3, 0.0, 1.0, None, None, 0, None) == 1
     assert lib.polsar_checksum(None, 5, 2, 1, 0, 0, None, None, None) == 1
     assert lib.polsar_inv_det_host(None, None, None, 5, 5, 0, 0, None, 0, None, None, None) == 1
-    assert lib.polsar_window_workspace_bytes(2048, 2048, 0) >= 2048 * 2048 * 4
+    assert lib.polsar_window_workspace_bytes(2048, 2048, 11, 0) >= 2048 * 2048 * (4 + 8 + 264 * 4)
     assert lib.polsar_host_chunk_pixels(3 << 30, 0) % 64 == 0
 
 

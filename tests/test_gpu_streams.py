@@ -18,7 +18,7 @@ def test_cuda_graph_capture_replay(cuda):
     st = torch.empty(z.shape[1], dtype=torch.uint8, device=cuda)
     c5 = configs.get("c5").scaled(64, 96)
     z5 = wishart.generate(c5, device=cuda)
-    ws = torch.empty(P.polsar_window_workspace_bytes(64, 96, 0), dtype=torch.uint8, device=cuda)
+    ws = torch.empty(P.polsar_window_workspace_bytes(64, 96, 11, 0), dtype=torch.uint8, device=cuda)
     w5 = torch.empty(64 * 96, dtype=z5.dtype, device=cuda)
     ref_out, ref_st = P.inv_det(z)
     ref_w = P.window_distance(z5, 64, 96)

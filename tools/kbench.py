@@ -43,7 +43,7 @@ def main():
             z = wishart.generate(c5, device=dev, stream=s)
             for plain in (False, True):
                 code = P.dtype_code(z.dtype, plain)
-                ws = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, code),
+                ws = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, c5.radius, code),
                                  dtype=torch.uint8, device=dev)
                 out = torch.empty(c5.n, dtype=z.dtype, device=dev)
                 ms = timeit(lambda: P.polsar_window_distance(z, c5.width, c5.height, 0, c5.height,
@@ -51,12 +51,12 @@ def main():
                                                              plain=plain, stream=s), s)
                 res[f"window_c5{'_plain' if plain else ''}_ms"] = ms
             z64 = z.double()
-            ws = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, 1),
+            ws = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, c5.radius, 1),
                              dtype=torch.uint8, device=dev)
             out = torch.empty(c5.n, dtype=z64.dtype, device=dev)
             zz = torch.empty((9, c5.n), dtype=z.dtype, device=dev)
             wo = torch.empty(c5.n, dtype=z.dtype, device=dev)
-            ws32 = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, 0),
+            ws32 = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, c5.radius, 0),
                                dtype=torch.uint8, device=dev)
             res["nlm_c5_ms"] = timeit(lambda: P.polsar_nlm_filter(z, c5.width, c5.height, 0, c5.height,
                                                                   c5.radius, c5.looks, c5.h, ws32, zz, wo,

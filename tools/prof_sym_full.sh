@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+NCU=/usr/local/cuda/bin/ncu
+CMD="python tools/kbench.py --what window"
+$CMD > gpurun_out/kb_sym.json 2>&1 && \
+$NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/sym_launches.csv $CMD > gpurun_out/sym_ncu.log 2>&1 && \
+$NCU --set full --import-source on --clock-control none -k regex:k_window_fwd -c 1 -o gpurun_out/fwd_full -f $CMD > gpurun_out/fwd_ncu.log 2>&1
+echo "rc=$?"
