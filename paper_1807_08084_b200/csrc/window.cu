@@ -96,6 +96,44 @@ __device__ __forceinline__ WT pair_w(const T* zi, WT gi, const T* zj, WT gj, WT 
     return pair_weight(rr, alpha, a2);
 }
 
+// Shared-memory halo pixel (symmetric pass 1, NLM): the 9 planes and g in one 10-slot record
+// (stride 10 T: 16-byte aligned for T = double, 8-byte for float), read with
+// five 2-wide loads from one address.  Record strides of 5 (double2) / 5
+// (float2) bank units are odd, so a warp's loads are conflict-free.
+template <typename T>
+struct Vec2Of;
+template <>
+struct Vec2Of<double> { using type = double2; };
+template <>
+struct Vec2Of<float> { using type = float2; };
+
+// g (WT) carried in the record's T slot, bit-exact.
+template <typename T, typename WT>
+__device__ __forceinline__ T pack_g(WT v) {
+    if constexpr (sizeof(T) == sizeof(WT)) return (T)v;
+    else return __longlong_as_double((long long)__float_as_uint(v));
+}
+template <typename T, typename WT>
+__device__ __forceinline__ WT unpack_g(T v) {
+    if constexpr (sizeof(T) == sizeof(WT)) return (WT)v;
+    else return __uint_as_float((unsigned)__double_as_longlong(v));
+}
+
+template <typename T, typename WT>
+__device__ __forceinline__ void load_rec(const T* rec, T (&zj)[9], WT& gj) {
+    using V = typename Vec2Of<T>::type;
+    const V* p = reinterpret_cast<const V*>(rec);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const V v = p[k];
+        zj[2 * k] = v.x;
+        zj[2 * k + 1] = v.y;
+    }
+    const V v = p[4];
+    zj[8] = v.x;
+    gj = unpack_g<T, WT>(v.y);
+}
+
 #ifndef POLSAR_K3_RB
 #define POLSAR_K3_RB 2
 #endif
@@ -273,12 +311,11 @@ __global__ void __launch_bounds__(K3_TX * TY / RB, 1)
 k_nlm_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
           int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
           int alpha_is_2, S* __restrict__ out_w, S* __restrict__ out_z, int64_t ld_out) {
-    extern __shared__ unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const int HW = K3_TX + 2 * R;
     const int HH = TY + 2 * R;
     const int HP = HW * HH;
-    T* sz = reinterpret_cast<T*>(smem_raw);
-    WT* sg = reinterpret_cast<WT*>(sz + 9 * HP);
+    T* sz = reinterpret_cast<T*>(smem_raw);  // HP records of 10 T (load_rec)
 
     const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
     const int64_t y0 = row_begin + (int64_t)blockIdx.y * TY;
@@ -287,9 +324,10 @@ k_nlm_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
         int64_t gy = y0 - R + hy, gx = x0 - R + hx;
         bool in = gy >= 0 && gy < slab_rows && gx >= 0 && gx < width;
         int64_t p = in ? gy * width + gx : 0;
+        T* rec = sz + 10 * q;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) sz[k * HP + q] = in ? (T)z[k * ld + p] : T(0);
-        sg[q] = in ? g[p] : WT(0);
+        for (int k = 0; k < 9; ++k) rec[k] = in ? (T)z[k * ld + p] : T(0);
+        rec[9] = pack_g<T, WT>(in ? g[p] : WT(0));
     }
     __syncthreads();
 
@@ -300,13 +338,9 @@ k_nlm_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
     WT gi[RB];
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-        int q = (ty0 + r + R) * HW + (tx + R);
+        load_rec(sz + 10 * ((ty0 + r + R) * HW + (tx + R)), zi[r], gi[r]);
 #pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            zi[r][k] = sz[k * HP + q];
-            accz[r][k] = T(0);
-        }
-        gi[r] = sg[q];
+        for (int k = 0; k < 9; ++k) accz[r][k] = T(0);
         accw[r] = T(0);
     }
     const WT alpha = (WT)alpha_d;
@@ -317,17 +351,15 @@ k_nlm_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
         const int64_t gyj = y0 + ty0 + wy;
         if (gyj < 0 || gyj >= slab_rows) continue;  // warp-uniform
         const int hy = ty0 + wy + R;
-        const T* rowz = sz + hy * HW + tx + R;
-        const WT* rowg = sg + hy * HW + tx + R;
+        const T* rec = sz + 10 * (hy * HW + tx);  // neighbour wx = -R
         bool rok[RB];
 #pragma unroll
         for (int r = 0; r < RB; ++r) rok[r] = (wy - r >= -R) && (wy - r <= R);  // warp-uniform
-        for (int wx = -R; wx <= R; ++wx) {
+        for (int wx = -R; wx <= R; ++wx, rec += 10) {
             T zj[9];
+            WT gj;
             POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-#pragma unroll
-            for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
-            const WT gj = rowg[wx];
+            load_rec(rec, zj, gj);
             const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
 #pragma unroll
             for (int r = 0; r < RB; ++r) {
@@ -362,12 +394,12 @@ int launch_nlm(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int
     const int64_t n = slab_rows * width;
     k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
     const double alpha = looks / (2.0 * h);
-    dim3 block(K3_TX * 16 / 2);
+    auto nlm_smem = [R](int ty) { return (size_t)(K3_TX + 2 * R) * (ty + 2 * R) * 10 * sizeof(T); };
     int TY = 16;
-    size_t smem = window_smem<T, WT>(16, R);
+    size_t smem = nlm_smem(16);
     if (smem > K3_SMEM_MAX) {
         TY = 8;
-        smem = window_smem<T, WT>(8, R);
+        smem = nlm_smem(8);
         if (smem > K3_SMEM_MAX)
             return fail(POLSAR_ENOTSUP, "polsar_nlm_filter: radius too large for shared memory");
     }
@@ -810,44 +842,16 @@ __device__ __forceinline__ int fwd_index(int dy, int dx, int R) {
     return dy == 0 ? dx - 1 : R + (dy - 1) * (2 * R + 1) + (dx + R);
 }
 
-// Shared-memory halo pixel of pass 1: the 9 planes and g in one 10-slot record
-// (stride 10 T: 16-byte aligned for T = double, 8-byte for float), read with
-// five 2-wide loads from one address.  Record strides of 5 (double2) / 5
-// (float2) bank units are odd, so a warp's loads are conflict-free.
-template <typename T>
-struct Vec2Of;
-template <>
-struct Vec2Of<double> { using type = double2; };
-template <>
-struct Vec2Of<float> { using type = float2; };
-
-// g (WT) carried in the record's T slot, bit-exact.
-template <typename T, typename WT>
-__device__ __forceinline__ T pack_g(WT v) {
-    if constexpr (sizeof(T) == sizeof(WT)) return (T)v;
-    else return __longlong_as_double((long long)__float_as_uint(v));
-}
-template <typename T, typename WT>
-__device__ __forceinline__ WT unpack_g(T v) {
-    if constexpr (sizeof(T) == sizeof(WT)) return (WT)v;
-    else return __uint_as_float((unsigned)__double_as_longlong(v));
-}
-
-template <typename T, typename WT>
-__device__ __forceinline__ void load_rec(const T* rec, T (&zj)[9], WT& gj) {
-    using V = typename Vec2Of<T>::type;
-    const V* p = reinterpret_cast<const V*>(rec);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const V v = p[k];
-        zj[2 * k] = v.x;
-        zj[2 * k + 1] = v.y;
-    }
-    const V v = p[4];
-    zj[8] = v.x;
-    gj = unpack_g<T, WT>(v.y);
-}
-
+#ifndef POLSAR_SYM_TY
+#define POLSAR_SYM_TY 32
+#endif
+#ifndef POLSAR_SYM_RB
+#define POLSAR_SYM_RB 2
+#endif
+#ifndef POLSAR_SYM_UNROLL
+#define POLSAR_SYM_UNROLL 1
+#endif
+constexpr int kSymUnroll = POLSAR_SYM_UNROLL;
 template <typename S, typename T, typename WT, int TY, int RB>
 __global__ void __launch_bounds__(K3_TX * TY / RB, 1)
 k_window_fwd(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
@@ -909,6 +913,7 @@ k_window_fwd(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
             WT* wp[RB];
 #pragma unroll
             for (int r = 0; r < RB; ++r) wp[r] = wbuf + (int64_t)fwd_index(wy - r, -R, R) * N + pi[r];
+#pragma unroll kSymUnroll
             for (int wx = -R; wx <= R; ++wx, rec += 10) {
                 POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
                 T zj[9];
@@ -994,11 +999,12 @@ size_t window_sym_bytes(int64_t n, int R) {
     return up(n * sizeof(WT)) + up(n * sizeof(double)) + up((size_t)fwd_count(R) * n * sizeof(WT));
 }
 
+// Pass 1 of the symmetric form (prepass + forward weights).  Returns the
+// weight planes and F.
 template <typename S, typename T, typename WT>
-int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                      int64_t re, int R, double looks, double h, void* wsv, void* outv,
-                      cudaStream_t s) {
-    const S* z = (const S*)zv;
+int sym_pass1(const S* z, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re,
+              int R, double looks, double h, void* wsv, WT** wbuf_out, double** fbuf_out,
+              cudaStream_t s, const char* who) {
     const int64_t n = slab_rows * width;
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
     unsigned char* ws = (unsigned char*)wsv;
@@ -1010,19 +1016,34 @@ int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_ro
     // pass 1 covers the output rows and the R rows above them (their forward
     // pairs are the backward pairs of the first output rows)
     const int64_t p0 = rb - R > 0 ? rb - R : 0;
-    constexpr int TY = 32, RB = 2;
+    constexpr int TY = POLSAR_SYM_TY, RB = POLSAR_SYM_RB;
     const size_t smem = window_fwd_smem<T, WT>(TY, R);
     auto kern = k_window_fwd<S, T, WT, TY, RB>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
+        return fail(POLSAR_ENOTSUP, who);
     dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - p0 + TY - 1) / TY));
     kern<<<grid, K3_TX * TY / RB, smem, s>>>(z, ld, width, slab_rows, p0, re, R, g, alpha,
                                              alpha == 2.0 ? 1 : 0, wbuf, fbuf);
+    *wbuf_out = wbuf;
+    *fbuf_out = fbuf;
+    return POLSAR_OK;
+}
+
+template <typename S, typename T, typename WT>
+int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
+                      int64_t re, int R, double looks, double h, void* wsv, void* outv,
+                      cudaStream_t s) {
+    WT* wbuf;
+    double* fbuf;
+    int rc = sym_pass1<S, T, WT>((const S*)zv, ld, width, slab_rows, rb, re, R, looks, h, wsv, &wbuf,
+                                 &fbuf, s, "polsar_window_distance: shared memory request too large");
+    if (rc != POLSAR_OK) return rc;
     k_window_bwd<S, WT><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
         wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
     return launch_check("polsar_window_distance: launch failed");
 }
+
 
 }  // namespace
 }  // namespace polsar_impl
