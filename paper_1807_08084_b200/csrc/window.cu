@@ -957,11 +957,14 @@ k_window_fwd(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
 }
 
 // Pass 2: W_j = 1 + F_j + sum over backward neighbours, one thread per pixel.
-// Each (delta_y) row of weights is summed in WT, then added in double.
-template <typename S, typename WT>
+// Each (delta_y) row of weights is summed in WT, then added in double.  RC > 0
+// fixes R at compile time (the paper's R = 11), so a row's 2R+1 independent
+// loads are all in flight at once.
+template <typename S, typename WT, int RC>
 __global__ void __launch_bounds__(256)
 k_window_bwd(const WT* __restrict__ wbuf, const double* __restrict__ fbuf, int64_t width,
-             int64_t slab_rows, int64_t row_begin, int64_t row_end, int R, S* __restrict__ out) {
+             int64_t slab_rows, int64_t row_begin, int64_t row_end, int R_rt, S* __restrict__ out) {
+    const int R = RC > 0 ? RC : R_rt;
     const int64_t N = slab_rows * width;
     const int64_t m = (row_end - row_begin) * width;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
@@ -976,7 +979,12 @@ k_window_bwd(const WT* __restrict__ wbuf, const double* __restrict__ fbuf, int64
             const WT* base = wbuf + (int64_t)fwd_index(dy, dx0, R) * N + p - (int64_t)dy * width - dx0;
             WT rowp = WT(0);
             if (inx) {
-                for (int dx = dx0; dx <= R; ++dx) rowp += base[(int64_t)(dx - dx0) * (N - 1)];
+                if (RC > 0 && dy > 0) {
+#pragma unroll
+                    for (int k = 0; k < 2 * RC + 1; ++k) rowp += base[(int64_t)k * (N - 1)];
+                } else {
+                    for (int dx = dx0; dx <= R; ++dx) rowp += base[(int64_t)(dx - dx0) * (N - 1)];
+                }
             } else {
                 for (int dx = dx0; dx <= R; ++dx)
                     if (x - dx >= 0 && x - dx < width) rowp += base[(int64_t)(dx - dx0) * (N - 1)];
@@ -1039,8 +1047,12 @@ int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_ro
     int rc = sym_pass1<S, T, WT>((const S*)zv, ld, width, slab_rows, rb, re, R, looks, h, wsv, &wbuf,
                                  &fbuf, s, "polsar_window_distance: shared memory request too large");
     if (rc != POLSAR_OK) return rc;
-    k_window_bwd<S, WT><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
-        wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
+    if (R == 11)
+        k_window_bwd<S, WT, 11><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
+            wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
+    else
+        k_window_bwd<S, WT, 0><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
+            wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
     return launch_check("polsar_window_distance: launch failed");
 }
 
