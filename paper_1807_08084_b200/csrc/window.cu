@@ -852,17 +852,93 @@ __device__ __forceinline__ int fwd_index(int dy, int dx, int R) {
 #define POLSAR_SYM_UNROLL 1
 #endif
 constexpr int kSymUnroll = POLSAR_SYM_UNROLL;
-template <typename S, typename T, typename WT, int TY, int RB>
+
+// Pair policies of pass 1: what a shared-memory record holds (RS slots of T)
+// and how a pair weight is computed from two records.
+//
+// Log-det distance (R-12): 9 planes + g = 1/(8 det Z); w from Eq. 6 on
+// S = Z_i + Z_j (pair_w).
+template <typename S_, typename T_, typename WT_>
+struct LogDetPair {
+    using S = S_;
+    using T = T_;
+    using WT = WT_;
+    static constexpr int RS = 10;
+    struct Rec {
+        T z[9];
+        WT g;
+    };
+    const S* z;
+    int64_t ld;
+    const WT* g;
+    WT alpha;
+    bool a2;
+    __device__ __forceinline__ void fill(T* rec, int64_t p, bool in) const {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) rec[k] = in ? (T)z[k * ld + p] : T(0);
+        rec[9] = pack_g<T, WT>(in ? g[p] : WT(0));
+    }
+    __device__ __forceinline__ static void load(const T* rec, Rec& r) { load_rec(rec, r.z, r.g); }
+    __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
+        return pair_w<T, WT>(i.z, i.g, j.z, j.g, alpha, a2);
+    }
+};
+
+// Symmetric Wishart KL (K6): Z and X = w * Z^-1 (Alg. 2 in k_window_prep_kl,
+// w the Hermitian trace weights), T = <X_i, Z_j> + <Z_i, X_j>
+// = tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i), w = exp(-L (T/2 - 3) / h).
+template <typename WT_>
+struct KLPair {
+    using T = double;
+    using WT = WT_;
+    static constexpr int RS = 18;
+    struct Rec {
+        double z[9];
+        double x[9];
+    };
+    const double* ws;  // prep planes 0..8 = Z, 9..17 = X, plane stride P
+    int64_t P;
+    WT lk;             // L / h
+    __device__ __forceinline__ void fill(double* rec, int64_t p, bool in) const {
+#pragma unroll
+        for (int k = 0; k < 18; ++k) rec[k] = in ? ws[k * P + p] : 0.0;
+    }
+    __device__ __forceinline__ static void load(const double* rec, Rec& r) {
+        const double2* v = reinterpret_cast<const double2*>(rec);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            const double2 u = v[k];
+            const int a = 2 * k, b = 2 * k + 1;
+            (a < 9 ? r.z[a] : r.x[a - 9]) = u.x;
+            (b < 9 ? r.z[b] : r.x[b - 9]) = u.y;
+        }
+    }
+    __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
+        double A = __dmul_rn(i.x[0], j.z[0]);
+        double B = __dmul_rn(i.z[0], j.x[0]);
+#pragma unroll
+        for (int k = 1; k < 9; ++k) {
+            A = __fma_rn(i.x[k], j.z[k], A);
+            B = __fma_rn(i.z[k], j.x[k], B);
+        }
+        return weight_kl<WT>(__dadd_rn(A, B), lk);
+    }
+};
+
+// Pass 1, generic over the pair policy.
+template <typename Pair, int TY, int RB>
 __global__ void __launch_bounds__(K3_TX * TY / RB, 1)
-k_window_fwd(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
-             int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
-             int alpha_is_2, WT* __restrict__ wbuf, double* __restrict__ fbuf) {
-    static_assert(sizeof(WT) <= sizeof(T), "g must fit a T slot");
+k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64_t row_end, int R,
+             typename Pair::WT* __restrict__ wbuf, double* __restrict__ fbuf) {
+    using T = typename Pair::T;
+    using WT = typename Pair::WT;
+    using Rec = typename Pair::Rec;
+    constexpr int RS = Pair::RS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int HW = K3_TX + 2 * R;   // halo columns x0-R .. x0+TX-1+R
     const int HH = TY + R;          // halo rows y0 .. y0+TY-1+R (forward only)
     const int HP = HW * HH;
-    T* sz = reinterpret_cast<T*>(smem_raw);  // HP records of 10 T
+    T* sz = reinterpret_cast<T*>(smem_raw);  // HP records of RS T
     const int64_t N = slab_rows * width;
 
     const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
@@ -871,19 +947,14 @@ k_window_fwd(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
         int hy = q / HW, hx = q % HW;
         int64_t gy = y0 + hy, gx = x0 - R + hx;
         bool in = gy < slab_rows && gx >= 0 && gx < width;
-        int64_t p = in ? gy * width + gx : 0;
-        T* rec = sz + 10 * q;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) rec[k] = in ? (T)z[k * ld + p] : T(0);
-        rec[9] = pack_g<T, WT>(in ? g[p] : WT(0));
+        pr.fill(sz + RS * q, in ? gy * width + gx : 0, in);
     }
     __syncthreads();
 
     const int tx = threadIdx.x % K3_TX;
     const int ty0 = (threadIdx.x / K3_TX) * RB;
     const int64_t gx = x0 + tx;
-    T zi[RB][9];
-    WT gi[RB];
+    Rec ri[RB];
     double acc[RB];
     bool own[RB];
     int64_t pi[RB];
@@ -892,18 +963,16 @@ k_window_fwd(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
         const int64_t gy = y0 + ty0 + r;
         own[r] = gx < width && gy < row_end;
         pi[r] = gy * width + gx;
-        load_rec(sz + 10 * ((ty0 + r) * HW + (tx + R)), zi[r], gi[r]);
+        Pair::load(sz + RS * ((ty0 + r) * HW + (tx + R)), ri[r]);
         acc[r] = 0.0;
     }
-    const WT alpha = (WT)alpha_d;
-    const bool a2 = alpha_is_2 != 0;
     const bool interior_x = (x0 - R >= 0) && (x0 + K3_TX + R <= width);
 
     for (int wy = 0; wy <= R + RB - 1; ++wy) {
         const int64_t gyj = y0 + ty0 + wy;
         if (gyj >= slab_rows) break;  // warp-uniform
         const int hy = ty0 + wy;
-        const T* rec = sz + 10 * (hy * HW + tx);  // neighbour wx = -R
+        const T* rec = sz + RS * (hy * HW + tx);  // neighbour wx = -R
         WT row[RB];
 #pragma unroll
         for (int r = 0; r < RB; ++r) row[r] = WT(0);
@@ -914,15 +983,14 @@ k_window_fwd(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
 #pragma unroll
             for (int r = 0; r < RB; ++r) wp[r] = wbuf + (int64_t)fwd_index(wy - r, -R, R) * N + pi[r];
 #pragma unroll kSymUnroll
-            for (int wx = -R; wx <= R; ++wx, rec += 10) {
+            for (int wx = -R; wx <= R; ++wx, rec += RS) {
                 POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-                T zj[9];
-                WT gj;
-                load_rec(rec, zj, gj);
+                Rec rj;
+                Pair::load(rec, rj);
                 const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
 #pragma unroll
                 for (int r = 0; r < RB; ++r) {
-                    WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
+                    WT w = pr.weight(ri[r], rj);
                     w = colok ? w : WT(0);
                     row[r] += w;
                     if (colok && own[r]) *wp[r] = w;
@@ -930,17 +998,16 @@ k_window_fwd(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_ro
                 }
             }
         } else {
-            for (int wx = -R; wx <= R; ++wx, rec += 10) {
+            for (int wx = -R; wx <= R; ++wx, rec += RS) {
                 POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-                T zj[9];
-                WT gj;
-                load_rec(rec, zj, gj);
+                Rec rj;
+                Pair::load(rec, rj);
                 const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
 #pragma unroll
                 for (int r = 0; r < RB; ++r) {
                     const int dy = wy - r;
                     if (dy >= 0 && dy <= R && (dy > 0 || wx > 0)) {  // warp-uniform
-                        WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
+                        WT w = pr.weight(ri[r], rj);
                         w = colok ? w : WT(0);
                         row[r] += w;
                         if (colok && own[r]) wbuf[(int64_t)fwd_index(dy, wx, R) * N + pi[r]] = w;
@@ -995,9 +1062,36 @@ k_window_bwd(const WT* __restrict__ wbuf, const double* __restrict__ fbuf, int64
     }
 }
 
-template <typename T, typename WT>
+template <typename Pair>
 size_t window_fwd_smem(int TY, int R) {
-    return (size_t)(K3_TX + 2 * R) * (TY + R) * 10 * sizeof(T);
+    return (size_t)(K3_TX + 2 * R) * (TY + R) * Pair::RS * sizeof(typename Pair::T);
+}
+
+// Launch pass 1 over rows [p0, re) (p0 = max(0, rb - R): the R rows above the
+// output rows hold the forward pairs that are their backward pairs).
+template <typename Pair, int TY, int RB>
+int launch_fwd(const Pair& pr, int64_t width, int64_t slab_rows, int64_t rb, int64_t re, int R,
+               typename Pair::WT* wbuf, double* fbuf, cudaStream_t s, const char* who) {
+    const int64_t p0 = rb - R > 0 ? rb - R : 0;
+    const size_t smem = window_fwd_smem<Pair>(TY, R);
+    auto kern = k_window_fwd<Pair, TY, RB>;
+    if (smem > K3_SMEM_MAX ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return fail(POLSAR_ENOTSUP, who);
+    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - p0 + TY - 1) / TY));
+    kern<<<grid, K3_TX * TY / RB, smem, s>>>(pr, width, slab_rows, p0, re, R, wbuf, fbuf);
+    return POLSAR_OK;
+}
+
+template <typename S, typename WT>
+void launch_bwd(const WT* wbuf, const double* fbuf, int64_t width, int64_t slab_rows, int64_t rb,
+                int64_t re, int R, void* outv, cudaStream_t s) {
+    if (R == 11)
+        k_window_bwd<S, WT, 11><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
+            wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
+    else
+        k_window_bwd<S, WT, 0><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
+            wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
 }
 
 // workspace: g (N x WT) | F (N x double) | wbuf (fwd_count(R) x N x WT)
@@ -1007,12 +1101,11 @@ size_t window_sym_bytes(int64_t n, int R) {
     return up(n * sizeof(WT)) + up(n * sizeof(double)) + up((size_t)fwd_count(R) * n * sizeof(WT));
 }
 
-// Pass 1 of the symmetric form (prepass + forward weights).  Returns the
-// weight planes and F.
 template <typename S, typename T, typename WT>
-int sym_pass1(const S* z, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re,
-              int R, double looks, double h, void* wsv, WT** wbuf_out, double** fbuf_out,
-              cudaStream_t s, const char* who) {
+int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
+                      int64_t re, int R, double looks, double h, void* wsv, void* outv,
+                      cudaStream_t s) {
+    const S* z = (const S*)zv;
     const int64_t n = slab_rows * width;
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
     unsigned char* ws = (unsigned char*)wsv;
@@ -1021,41 +1114,41 @@ int sym_pass1(const S* z, int64_t ld, int64_t width, int64_t slab_rows, int64_t 
     WT* wbuf = (WT*)(ws + up(n * sizeof(WT)) + up(n * sizeof(double)));
     k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
     const double alpha = looks / (2.0 * h);
-    // pass 1 covers the output rows and the R rows above them (their forward
-    // pairs are the backward pairs of the first output rows)
-    const int64_t p0 = rb - R > 0 ? rb - R : 0;
-    constexpr int TY = POLSAR_SYM_TY, RB = POLSAR_SYM_RB;
-    const size_t smem = window_fwd_smem<T, WT>(TY, R);
-    auto kern = k_window_fwd<S, T, WT, TY, RB>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return fail(POLSAR_ENOTSUP, who);
-    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - p0 + TY - 1) / TY));
-    kern<<<grid, K3_TX * TY / RB, smem, s>>>(z, ld, width, slab_rows, p0, re, R, g, alpha,
-                                             alpha == 2.0 ? 1 : 0, wbuf, fbuf);
-    *wbuf_out = wbuf;
-    *fbuf_out = fbuf;
-    return POLSAR_OK;
-}
-
-template <typename S, typename T, typename WT>
-int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                      int64_t re, int R, double looks, double h, void* wsv, void* outv,
-                      cudaStream_t s) {
-    WT* wbuf;
-    double* fbuf;
-    int rc = sym_pass1<S, T, WT>((const S*)zv, ld, width, slab_rows, rb, re, R, looks, h, wsv, &wbuf,
-                                 &fbuf, s, "polsar_window_distance: shared memory request too large");
+    LogDetPair<S, T, WT> pr{z, ld, g, (WT)alpha, alpha == 2.0};
+    int rc = launch_fwd<LogDetPair<S, T, WT>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
+        pr, width, slab_rows, rb, re, R, wbuf, fbuf, s,
+        "polsar_window_distance: shared memory request too large");
     if (rc != POLSAR_OK) return rc;
-    if (R == 11)
-        k_window_bwd<S, WT, 11><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
-            wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
-    else
-        k_window_bwd<S, WT, 0><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
-            wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
+    launch_bwd<S, WT>(wbuf, fbuf, width, slab_rows, rb, re, R, outv, s);
     return launch_check("polsar_window_distance: launch failed");
 }
 
+// K6, symmetric form: the KL prepass planes | F | weight planes.
+template <typename WT>
+size_t kl_sym_bytes(int64_t n, int R) {
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    return up((size_t)n * V3_NP * sizeof(double)) + up(n * sizeof(double)) +
+           up((size_t)fwd_count(R) * n * sizeof(WT));
+}
+
+template <typename S, typename WT>
+int launch_window_kl_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
+                         int64_t re, int R, double looks, double h, void* wsv, void* outv,
+                         cudaStream_t s) {
+    const int64_t n = slab_rows * width;
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    unsigned char* ws = (unsigned char*)wsv;
+    double* prep = (double*)ws;
+    double* fbuf = (double*)(ws + up((size_t)n * V3_NP * sizeof(double)));
+    WT* wbuf = (WT*)(ws + up((size_t)n * V3_NP * sizeof(double)) + up(n * sizeof(double)));
+    k_window_prep_kl<S><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, prep);
+    KLPair<WT> pr{prep, n, (WT)(looks / h)};
+    int rc = launch_fwd<KLPair<WT>, 16, 2>(pr, width, slab_rows, rb, re, R, wbuf, fbuf, s,
+                                            "polsar_window_kl: shared memory request too large");
+    if (rc != POLSAR_OK) return rc;
+    launch_bwd<S, WT>(wbuf, fbuf, width, slab_rows, rb, re, R, outv, s);
+    return launch_check("polsar_window_kl: launch failed");
+}
 
 }  // namespace
 }  // namespace polsar_impl
@@ -1073,8 +1166,11 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radiu
     // symmetric form (g, F and 2R(R+1) weight planes)
     size_t b = (((size_t)n * (wt64 ? 8 : 4)) + 255) / 256 * 256;
     if (dtype != POLSAR_F32_PLAIN) b = std::max(b, ((size_t)n * 160 + 255) / 256 * 256);
-    if (radius <= V3_RMAX)
+    if (radius <= V3_RMAX) {
         b = std::max(b, wt64 ? window_sym_bytes<double>(n, radius) : window_sym_bytes<float>(n, radius));
+        if (dtype != POLSAR_F32_PLAIN)
+            b = std::max(b, wt64 ? kl_sym_bytes<double>(n, radius) : kl_sym_bytes<float>(n, radius));
+    }
     return b;
 }
 
@@ -1137,10 +1233,17 @@ int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows
     cudaStream_t s = (cudaStream_t)cuda_stream;
     switch (dtype) {
         case POLSAR_F32:
+            if (window_variant() == 4)
+                return launch_window_kl_sym<float, float>(z, ld, width, slab_rows, out_row_begin,
+                                                          out_row_end, radius, looks, h, workspace, out, s);
             return launch_window_kl<float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
                                                   radius, looks, h, workspace, out, s);
         case POLSAR_F64:
         case POLSAR_F64_PLAIN:
+            if (window_variant() == 4)
+                return launch_window_kl_sym<double, double>(z, ld, width, slab_rows, out_row_begin,
+                                                            out_row_end, radius, looks, h, workspace,
+                                                            out, s);
             return launch_window_kl<double, double>(z, ld, width, slab_rows, out_row_begin,
                                                     out_row_end, radius, looks, h, workspace, out, s);
         default: return fail(POLSAR_ENOTSUP, "polsar_window_kl: fp32-arithmetic mode not provided");

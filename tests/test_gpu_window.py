@@ -93,9 +93,12 @@ def test_window_c5_sampled(cuda):
     assert np.all(np.isfinite(got)) and got.min() >= 1 - 1e-6 and got.max() <= 529 + 1e-3
 
 
-def test_window_variant3_subprocess(cuda):
-    """The alternative expansion-form kernel (POLSAR_WINDOW_VARIANT=3, read
-    once per process) against the oracle, in a child process."""
+@pytest.mark.parametrize("variant", ["2", "3"])
+def test_window_variant_subprocess(cuda, variant):
+    """The alternative kernels (POLSAR_WINDOW_VARIANT=2: the direct form over
+    ordered pairs; 3: the expansion form; read once per process) against the
+    oracle in a child process: the log-det window sum, and the KL window sum
+    (both variants run KL on the streaming expansion kernel)."""
     import os
     import subprocess
     import sys
@@ -103,16 +106,21 @@ def test_window_variant3_subprocess(cuda):
 import numpy as np, torch, oracle
 import paper_1807_08084_b200 as P
 from paper_1807_08084_b200 import configs, wishart
-for dt, tol in ((torch.float32, 2e-5), (torch.float64, 4e-10)):
+# tolerances of test_gpu_window / test_gpu_kl (R-12, R-16)
+for dt, tol, tol_kl in ((torch.float32, 2e-5, 2e-5), (torch.float64, 4e-10, 2e-9)):
     h, w, r = 80, 70, 11
     z = wishart.generate(configs.get("c5").scaled(h, w), device="cuda").to(dt)
     got = P.window_distance(z, h, w, radius=r).cpu().numpy()
     ref = oracle.window(z.cpu().numpy(), h, w, r, 4.0, 1.0)
     e = float((np.abs(got - ref) / ref).max())
-    assert e <= tol, (dt, e)
+    assert e <= tol, ("window", dt, e)
+    got = P.window_kl(z, h, w, radius=r).cpu().numpy()
+    ref = oracle.window_kl(z.cpu().numpy(), h, w, r, 4.0, 1.0)
+    e = float((np.abs(got - ref) / ref).max())
+    assert e <= tol_kl, ("kl", dt, e)
 print("ok")
 '''
-    env = dict(os.environ, POLSAR_WINDOW_VARIANT="3")
+    env = dict(os.environ, POLSAR_WINDOW_VARIANT=variant)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=300)
