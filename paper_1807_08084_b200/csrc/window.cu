@@ -879,8 +879,24 @@ struct LogDetPair {
         rec[9] = pack_g<T, WT>(in ? g[p] : WT(0));
     }
     __device__ __forceinline__ static void load(const T* rec, Rec& r) { load_rec(rec, r.z, r.g); }
+    // weight = post(pre(i, j), i, aux(j)): pre is the FP64 part (det of
+    // S = Z_i + Z_j by Eq. 6), post the fp32 weight (same arithmetic as pair_w)
+    static constexpr bool kPipeline = false;  // measured: pipelining costs 4 % here
+    using Q = T;
+    using Aux = WT;
+    __device__ __forceinline__ Q pre(const Rec& i, const Rec& j) const {
+        return det_eq6<T>(ADD(i.z[0], j.z[0]), ADD(i.z[1], j.z[1]), ADD(i.z[2], j.z[2]),
+                          ADD(i.z[3], j.z[3]), ADD(i.z[4], j.z[4]), ADD(i.z[5], j.z[5]),
+                          ADD(i.z[6], j.z[6]), ADD(i.z[7], j.z[7]), ADD(i.z[8], j.z[8]));
+    }
+    __device__ __forceinline__ static Aux aux(const Rec& j) { return j.g; }
+    __device__ __forceinline__ WT post(Q ds, const Rec& i, Aux gj) const {
+        WT fds = (WT)ds;
+        WT rr = (fds * i.g) * (fds * gj);
+        return pair_weight(rr, alpha, a2);
+    }
     __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
-        return pair_w<T, WT>(i.z, i.g, j.z, j.g, alpha, a2);
+        return post(pre(i, j), i, aux(j));
     }
 };
 
@@ -913,7 +929,10 @@ struct KLPair {
             (b < 9 ? r.z[b] : r.x[b - 9]) = u.y;
         }
     }
-    __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
+    static constexpr bool kPipeline = true;  // measured: 4.79 -> 4.43 ms on c5
+    using Q = double;
+    using Aux = int;
+    __device__ __forceinline__ Q pre(const Rec& i, const Rec& j) const {
         double A = __dmul_rn(i.x[0], j.z[0]);
         double B = __dmul_rn(i.z[0], j.x[0]);
 #pragma unroll
@@ -921,9 +940,87 @@ struct KLPair {
             A = __fma_rn(i.x[k], j.z[k], A);
             B = __fma_rn(i.z[k], j.x[k], B);
         }
-        return weight_kl<WT>(__dadd_rn(A, B), lk);
+        return __dadd_rn(A, B);
+    }
+    __device__ __forceinline__ static Aux aux(const Rec&) { return 0; }
+    __device__ __forceinline__ WT post(Q T, const Rec&, Aux) const { return weight_kl<WT>(T, lk); }
+    __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
+        return post(pre(i, j), i, aux(j));
     }
 };
+
+// Pass 1, one full window row (all 2R+1 neighbours valid for every owned
+// row): weights into row[] and, for owned in-image pairs, into the planes
+// wp[r] (advanced by one plane per neighbour).
+template <typename Pair, int RB>
+__device__ __forceinline__ void fwd_full_row(const Pair& pr, const typename Pair::Rec (&ri)[RB],
+                                             const typename Pair::T* rec, int R, int64_t gx,
+                                             int64_t width, bool interior_x, const bool (&own)[RB],
+                                             typename Pair::WT* (&wp)[RB], int64_t N,
+                                             typename Pair::WT (&row)[RB]) {
+    using WT = typename Pair::WT;
+#pragma unroll kSymUnroll
+    for (int wx = -R; wx <= R; ++wx, rec += Pair::RS) {
+        typename Pair::Rec rj;
+        Pair::load(rec, rj);
+        const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            WT w = pr.weight(ri[r], rj);
+            w = colok ? w : WT(0);
+            row[r] += w;
+            if (colok && own[r]) *wp[r] = w;
+            wp[r] += N;
+        }
+    }
+}
+
+// The same row software-pipelined by one neighbour: the FP64 part (pre) of
+// neighbour wx and the weight, sum and store (post) of wx - 1 form one basic
+// block, so the scheduler overlaps them.  The first post is a no-op
+// (ok = false) and the sums keep wx order, so results equal fwd_full_row's.
+template <typename Pair, int RB>
+__device__ __forceinline__ void fwd_full_row_pipelined(
+    const Pair& pr, const typename Pair::Rec (&ri)[RB], const typename Pair::T* rec, int R,
+    int64_t gx, int64_t width, bool interior_x, const bool (&own)[RB], typename Pair::WT* (&wp)[RB],
+    int64_t N, typename Pair::WT (&row)[RB]) {
+    using WT = typename Pair::WT;
+    typename Pair::Q qp[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        wp[r] -= N;
+        qp[r] = typename Pair::Q(1);
+    }
+    typename Pair::Aux ap = Pair::aux(ri[0]);
+    bool okp = false;
+#pragma unroll kSymUnroll
+    for (int wx = -R; wx <= R; ++wx, rec += Pair::RS) {
+        typename Pair::Rec rj;
+        Pair::load(rec, rj);
+        const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+        typename Pair::Q q[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) q[r] = pr.pre(ri[r], rj);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            WT w = pr.post(qp[r], ri[r], ap);
+            w = okp ? w : WT(0);
+            row[r] += w;
+            if (okp && own[r]) *wp[r] = w;
+            wp[r] += N;
+            qp[r] = q[r];
+        }
+        ap = Pair::aux(rj);
+        okp = colok;
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {  // the last neighbour's post
+        WT w = pr.post(qp[r], ri[r], ap);
+        w = okp ? w : WT(0);
+        row[r] += w;
+        if (okp && own[r]) *wp[r] = w;
+    }
+}
 
 // Pass 1, generic over the pair policy.
 template <typename Pair, int TY, int RB>
@@ -982,21 +1079,11 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
             WT* wp[RB];
 #pragma unroll
             for (int r = 0; r < RB; ++r) wp[r] = wbuf + (int64_t)fwd_index(wy - r, -R, R) * N + pi[r];
-#pragma unroll kSymUnroll
-            for (int wx = -R; wx <= R; ++wx, rec += RS) {
-                POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-                Rec rj;
-                Pair::load(rec, rj);
-                const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-#pragma unroll
-                for (int r = 0; r < RB; ++r) {
-                    WT w = pr.weight(ri[r], rj);
-                    w = colok ? w : WT(0);
-                    row[r] += w;
-                    if (colok && own[r]) *wp[r] = w;
-                    wp[r] += N;
-                }
-            }
+            POLSAR_CHECK(hy >= 0 && hy < HH && tx + 2 * R < HW);  // records wx = -R..R
+            if constexpr (Pair::kPipeline)
+                fwd_full_row_pipelined<Pair, RB>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row);
+            else
+                fwd_full_row<Pair, RB>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row);
         } else {
             for (int wx = -R; wx <= R; ++wx, rec += RS) {
                 POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
