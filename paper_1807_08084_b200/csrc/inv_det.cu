@@ -138,11 +138,176 @@ k_inv_det_scalar(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restri
 }
 
 
+// ------------------------------------------------ K1 / K2, bulk-copy form
+// SURVEY §8(a) row A1, reading (ii): literally one matrix per thread, with
+// the CTA staging each plane's tile through shared memory by the bulk-copy
+// engine (cp.async.bulk, completion on an mbarrier) and writing the 11 output
+// planes + status back with bulk stores.  Persistent: one CTA of KB_THREADS
+// per SM walks tiles of TP pixels; 3 input stages and 2 output buffers keep
+// ~200 KB in flight per SM.  Selected by POLSAR_K1_VARIANT=bulk (A/B; the
+// register-vector form above is the default, DESIGN.md §6 has both numbers).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int KB_THREADS = 512;
+constexpr int KB_NS = 3;  // input stages
+constexpr int KB_NO = 2;  // output buffers
+template <typename S>
+struct BulkTile {
+    static constexpr int TP = 4096 / sizeof(S);  // pixels per tile: 4 KB per plane
+};
+template <typename S>
+constexpr size_t bulk_smem_bytes() {
+    constexpr int TP = BulkTile<S>::TP;
+    return (size_t)KB_NS * 9 * TP * sizeof(S) + (size_t)KB_NO * 11 * TP * sizeof(S) + (size_t)KB_NO * TP +
+           KB_NS * sizeof(uint64_t);
+}
+
+template <typename S, int ALGO, int MATH>
+__global__ void __launch_bounds__(KB_THREADS, 1)
+k_inv_det_bulk(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
+               int64_t n_tiles, int64_t ld) {
+    constexpr int TP = BulkTile<S>::TP;
+    constexpr int PPT = TP / KB_THREADS;  // pixels per thread per tile
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    S* sin = reinterpret_cast<S*>(smem_raw);                    // [KB_NS][9][TP]
+    S* sout = sin + KB_NS * 9 * TP;                             // [KB_NO][11][TP]
+    uint8_t* sst = reinterpret_cast<uint8_t*>(sout + KB_NO * 11 * TP);  // [KB_NO][TP]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sst + KB_NO * TP);     // [KB_NS]
+    const int tid = threadIdx.x;
+    constexpr uint32_t plane_bytes = TP * sizeof(S);
+    if (tid == 0) {
+        for (int s = 0; s < KB_NS; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t step = gridDim.x;
+    auto issue_load = [&](int64_t t, int s) {
+        mbar_expect_tx(&bar[s], 9 * plane_bytes);
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+            bulk_g2s(sin + (s * 9 + k) * TP, z + k * ld + t * TP, plane_bytes, &bar[s]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < KB_NS; ++s) {
+            const int64_t t = blockIdx.x + s * step;
+            if (t < n_tiles) issue_load(t, s);
+        }
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += step, ++i) {
+        const int s = i % KB_NS;
+        const int ob = i % KB_NO;
+        mbar_wait(&bar[s], (uint32_t)(i / KB_NS) & 1u);
+#pragma unroll
+        for (int v = 0; v < PPT; ++v) {
+            const int q = tid + v * KB_THREADS;
+            POLSAR_CHECK(q < TP);
+            S x[9], y[11];
+            uint8_t st;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) x[k] = sin[(s * 9 + k) * TP + q];
+            solve_one<S, ALGO, MATH>(x, y, st);
+#pragma unroll
+            for (int k = 0; k < 11; ++k) sout[(ob * 11 + k) * TP + q] = y[k];
+            sst[ob * TP + q] = st;
+        }
+        // make the generic-proxy smem writes visible to the bulk (async) proxy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < 11; ++k) bulk_s2g(out + k * ld + t * TP, sout + (ob * 11 + k) * TP, plane_bytes);
+            if (status) bulk_s2g(status + t * TP, sst + ob * TP, TP);
+            bulk_commit();
+            const int64_t tn = t + KB_NS * step;  // stage s is free: every thread has read it
+            if (tn < n_tiles) issue_load(tn, s);
+            bulk_wait_read<KB_NO - 1>();  // the next tile's output buffer has been read out
+        }
+        __syncthreads();
+    }
+    if (tid == 0) bulk_wait<0>();
+}
+
+int k1_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("POLSAR_K1_VARIANT");
+        v = (e && e[0] == 'b') ? 1 : 0;
+    }
+    return v;
+}
+
+// Bulk form over the whole tiles of [0, n); returns the pixels it covers
+// (0 when the layout does not allow 16-byte bulk copies).
+template <typename S, int ALGO, int MATH>
+int64_t launch_bulk(const S* z, S* out, uint8_t* status, int64_t n, int64_t ld, cudaStream_t s) {
+    constexpr int TP = BulkTile<S>::TP;
+    const bool ok = ((uintptr_t)z % 16 == 0) && ((uintptr_t)out % 16 == 0) && ((ld * sizeof(S)) % 16 == 0) &&
+                    (status == nullptr || (uintptr_t)status % 16 == 0);
+    const int64_t n_tiles = ok ? n / TP : 0;
+    if (n_tiles == 0) return 0;
+    constexpr size_t smem = bulk_smem_bytes<S>();
+    auto kern = k_inv_det_bulk<S, ALGO, MATH>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return 0;
+        attr = true;
+    }
+    const int64_t grid = n_tiles < num_sms() ? n_tiles : num_sms();
+    kern<<<(unsigned)grid, KB_THREADS, smem, s>>>(z, out, status, n_tiles, ld);
+    return n_tiles * TP;
+}
+
 template <typename S, int ALGO, int MATH>
 int launch_inv_det(const void* zv, void* outv, uint8_t* status, int64_t n, int64_t ld,
                    cudaStream_t s) {
-    const S* z = (const S*)zv;
-    S* out = (S*)outv;
+    const S* z0 = (const S*)zv;
+    S* out0 = (S*)outv;
+    // optional bulk-copy form over whole tiles; the rest by the vector form
+    const int64_t nb = k1_variant() == 1 ? launch_bulk<S, ALGO, MATH>(z0, out0, status, n, ld, s) : 0;
+    const S* z = z0 + nb;
+    S* out = out0 + nb;
+    if (status) status += nb;
+    n -= nb;
     constexpr int W = VecSel<S, ALGO>::V::n;
     bool aligned = ((uintptr_t)z % 16 == 0) && ((uintptr_t)out % 16 == 0) && (ld % W == 0) &&
                    (status == nullptr || (uintptr_t)status % W == 0);

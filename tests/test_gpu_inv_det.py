@@ -213,3 +213,41 @@ def test_host_pipeline_matches_device(c2, dt, algo):
     torch.cuda.synchronize()
     assert torch.equal(oh, dev_out.cpu())
     assert torch.equal(sh, dev_st.cpu())
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_bulk_copy_variant_bit_identical(cuda, dt, tmp_path):
+    """The bulk-copy form of K1/K2 (POLSAR_K1_VARIANT=bulk, SURVEY §8(a) A1
+    reading (ii); read once per process) runs the same per-pixel arithmetic,
+    so its outputs and status equal the default form's bit for bit, across
+    whole tiles and a ragged tail handled by the vector form."""
+    import subprocess
+    import sys
+    n = 3 * 4096 + 1000 + 3
+    code = f'''
+import numpy as np, torch
+import paper_1807_08084_b200 as P
+from paper_1807_08084_b200 import configs, wishart
+z = wishart.generate(configs.get("c2").scaled(1, {n}), device="cuda").to(torch.{str(dt).split(".")[1]})
+res = {{}}
+for algo in ("adjugate", "cholesky"):
+    for plain in (False, True):
+        out, st = P.inv_det(z, algo=algo, plain=plain)
+        res[f"{{algo}}_{{plain}}"] = out.cpu().numpy()
+        res[f"{{algo}}_{{plain}}_st"] = st.cpu().numpy()
+np.savez(r"{tmp_path / 'bulk.npz'}", **res)
+print("ok")
+'''
+    env = dict(os.environ, POLSAR_K1_VARIANT="bulk")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+    got = np.load(tmp_path / "bulk.npz")
+    z = wishart.generate(configs.get("c2").scaled(1, n), device=cuda).to(dt)
+    for algo in ("adjugate", "cholesky"):
+        for plain in (False, True):
+            out, st = P.inv_det(z, algo=algo, plain=plain)
+            a, b = out.cpu().numpy(), got[f"{algo}_{plain}"]
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (algo, plain)
+            assert np.array_equal(st.cpu().numpy(), got[f"{algo}_{plain}_st"]), (algo, plain)
