@@ -5,6 +5,8 @@
 //   K3  polsar_window_distance   23x23 search-window log-det distance sum
 //   K4  polsar_nlm_filter        fused NLM filter output
 //   K6  polsar_window_kl         window sum with the symmetric Wishart KL distance
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -838,6 +840,14 @@ int window_variant() {
 // fixed order, so results are bit-reproducible and slab decompositions are
 // exact.
 __host__ __device__ __forceinline__ int fwd_count(int R) { return 2 * R * (R + 1); }
+// Row pitch of the weight planes: width rounded up to 16 bytes, so every row
+// of every plane starts 16-byte aligned (the TMA tiles of the NLM gather need
+// 16-byte aligned starts: measured, tools/micro/tma1d_test.cu).
+template <typename WT>
+__host__ __device__ __forceinline__ int64_t weight_pitch(int64_t width) {
+    constexpr int64_t a = 16 / sizeof(WT);
+    return (width + a - 1) / a * a;
+}
 __device__ __forceinline__ int fwd_index(int dy, int dx, int R) {
     return dy == 0 ? dx - 1 : R + (dy - 1) * (2 * R + 1) + (dx + R);
 }
@@ -1026,7 +1036,7 @@ __device__ __forceinline__ void fwd_full_row_pipelined(
 template <typename Pair, int TY, int RB>
 __global__ void __launch_bounds__(K3_TX * TY / RB, 1)
 k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64_t row_end, int R,
-             typename Pair::WT* __restrict__ wbuf, double* __restrict__ fbuf) {
+             int64_t wpitch, typename Pair::WT* __restrict__ wbuf, double* __restrict__ fbuf) {
     using T = typename Pair::T;
     using WT = typename Pair::WT;
     using Rec = typename Pair::Rec;
@@ -1036,7 +1046,7 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
     const int HH = TY + R;          // halo rows y0 .. y0+TY-1+R (forward only)
     const int HP = HW * HH;
     T* sz = reinterpret_cast<T*>(smem_raw);  // HP records of RS T
-    const int64_t N = slab_rows * width;
+    const int64_t N = slab_rows * wpitch;    // weight-plane stride (row pitch wpitch >= width)
 
     const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
     const int64_t y0 = row_begin + (int64_t)blockIdx.y * TY;
@@ -1054,12 +1064,12 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
     Rec ri[RB];
     double acc[RB];
     bool own[RB];
-    int64_t pi[RB];
+    int64_t pi[RB];  // weight-plane index of the owned pixel (F is indexed gy * width + gx)
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
         const int64_t gy = y0 + ty0 + r;
         own[r] = gx < width && gy < row_end;
-        pi[r] = gy * width + gx;
+        pi[r] = gy * wpitch + gx;
         Pair::load(sz + RS * ((ty0 + r) * HW + (tx + R)), ri[r]);
         acc[r] = 0.0;
     }
@@ -1107,7 +1117,7 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
     }
 #pragma unroll
     for (int r = 0; r < RB; ++r)
-        if (gx < width && y0 + ty0 + r < row_end) fbuf[pi[r]] = acc[r];
+        if (gx < width && y0 + ty0 + r < row_end) fbuf[(y0 + ty0 + r) * width + gx] = acc[r];
 }
 
 // Pass 2: W_j = 1 + F_j + sum over backward neighbours, one thread per pixel.
@@ -1117,9 +1127,10 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
 template <typename S, typename WT, int RC>
 __global__ void __launch_bounds__(256)
 k_window_bwd(const WT* __restrict__ wbuf, const double* __restrict__ fbuf, int64_t width,
-             int64_t slab_rows, int64_t row_begin, int64_t row_end, int R_rt, S* __restrict__ out) {
+             int64_t wpitch, int64_t slab_rows, int64_t row_begin, int64_t row_end, int R_rt,
+             S* __restrict__ out) {
     const int R = RC > 0 ? RC : R_rt;
-    const int64_t N = slab_rows * width;
+    const int64_t N = slab_rows * wpitch;  // weight-plane stride
     const int64_t m = (row_end - row_begin) * width;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
          q += (int64_t)gridDim.x * blockDim.x) {
@@ -1130,7 +1141,7 @@ k_window_bwd(const WT* __restrict__ wbuf, const double* __restrict__ fbuf, int64
         for (int dy = 0; dy <= R; ++dy) {
             if (y - dy < 0) break;
             const int dx0 = dy == 0 ? 1 : -R;
-            const WT* base = wbuf + (int64_t)fwd_index(dy, dx0, R) * N + p - (int64_t)dy * width - dx0;
+            const WT* base = wbuf + (int64_t)fwd_index(dy, dx0, R) * N + (y - dy) * wpitch + x - dx0;
             WT rowp = WT(0);
             if (inx) {
                 if (RC > 0 && dy > 0) {
@@ -1166,7 +1177,8 @@ int launch_fwd(const Pair& pr, int64_t width, int64_t slab_rows, int64_t rb, int
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return fail(POLSAR_ENOTSUP, who);
     dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - p0 + TY - 1) / TY));
-    kern<<<grid, K3_TX * TY / RB, smem, s>>>(pr, width, slab_rows, p0, re, R, wbuf, fbuf);
+    kern<<<grid, K3_TX * TY / RB, smem, s>>>(pr, width, slab_rows, p0, re, R, weight_pitch<typename Pair::WT>(width),
+                                             wbuf, fbuf);
     return POLSAR_OK;
 }
 
@@ -1175,17 +1187,20 @@ void launch_bwd(const WT* wbuf, const double* fbuf, int64_t width, int64_t slab_
                 int64_t re, int R, void* outv, cudaStream_t s) {
     if (R == 11)
         k_window_bwd<S, WT, 11><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
-            wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
+            wbuf, fbuf, width, weight_pitch<WT>(width), slab_rows, rb, re, R, (S*)outv);
     else
         k_window_bwd<S, WT, 0><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
-            wbuf, fbuf, width, slab_rows, rb, re, R, (S*)outv);
+            wbuf, fbuf, width, weight_pitch<WT>(width), slab_rows, rb, re, R, (S*)outv);
 }
 
-// workspace: g (N x WT) | F (N x double) | wbuf (fwd_count(R) x N x WT)
+// workspace: g (N x WT) | F (N x double) | wbuf (fwd_count(R) weight planes
+// of slab_rows x weight_pitch(width) WT; see weight_pitch)
 template <typename WT>
-size_t window_sym_bytes(int64_t n, int R) {
+size_t window_sym_bytes(int64_t slab_rows, int64_t width, int R) {
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-    return up(n * sizeof(WT)) + up(n * sizeof(double)) + up((size_t)fwd_count(R) * n * sizeof(WT));
+    const int64_t n = slab_rows * width;
+    return up(n * sizeof(WT)) + up(n * sizeof(double)) +
+           up((size_t)fwd_count(R) * slab_rows * weight_pitch<WT>(width) * sizeof(WT));
 }
 
 template <typename S, typename T, typename WT>
@@ -1212,10 +1227,11 @@ int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_ro
 
 // K6, symmetric form: the KL prepass planes | F | weight planes.
 template <typename WT>
-size_t kl_sym_bytes(int64_t n, int R) {
+size_t kl_sym_bytes(int64_t slab_rows, int64_t width, int R) {
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    const int64_t n = slab_rows * width;
     return up((size_t)n * V3_NP * sizeof(double)) + up(n * sizeof(double)) +
-           up((size_t)fwd_count(R) * n * sizeof(WT));
+           up((size_t)fwd_count(R) * slab_rows * weight_pitch<WT>(width) * sizeof(WT));
 }
 
 template <typename S, typename WT>
@@ -1237,6 +1253,352 @@ int launch_window_kl_sym(const void* zv, int64_t ld, int64_t width, int64_t slab
     return launch_check("polsar_window_kl: launch failed");
 }
 
+// ------------------------------------------------------------------------
+// K4, symmetric form (default for R <= V3_RMAX): pass 1 (k_window_fwd with
+// the log-det pair policy) stores every unordered pair's weight once; this
+// gather pass then forms, for every output pixel i,
+//   W_i = sum_j w_ij,   Zhat_i = sum_j w_ij Z_j / W_i
+// reading w_ij from the weight planes: with j = i + (dy, dx),
+//   forward  (dy > 0, or dy = 0 and dx > 0): w_ij = wbuf[fwd_index(dy, dx)][i]
+//   backward (the mirror):                   w_ij = wbuf[fwd_index(-dy, -dx)][j]
+//   j = i:                                   w_ii = 1 (d_ii = 0)
+// Along a neighbour row both offsets are linear in dx: forward
+// fwd_index(dy, 0) N + i + dx N, backward fwd_index(-dy, 0) N + j0 + dx (1 - N)
+// (j0 = the neighbour at dx = 0; for dy = 0, fwd_index(0, 0) = -1 and j0 = i).
+// So the pass is pure data movement plus 9 FMAs per ordered pair in the
+// storage precision: no FP64 determinant work at all (the direct form
+// k_nlm_sum evaluates every ordered pair's determinant, 29 FP64 ops, plus 10
+// FP64 accumulations).
+//
+// A CTA owns NLM_COLS = NLM_TX - AL columns x RB rows (AL = 16 / sizeof(WT));
+// each thread one column and RB rows, and the CTA walks the window rows its
+// pixels share.  For each window row:
+//  * the weights: for every owned row r and dx, the CTA's weights form one
+//    contiguous run of a weight plane (at i for forward pairs, at j = i +
+//    (dy, dx) for backward ones), fetched by TMA as one 1-D tile of NLM_TX
+//    elements of a tensor map over the whole weight buffer.  TMA needs a
+//    16-byte aligned start (measured, tools/micro/tma1d_test.cu); with the
+//    padded plane layout (weight_pitch) forward runs start aligned and a
+//    backward run at dx starts m(dx) = dx mod AL elements past an aligned
+//    point, so its tile is fetched from there and read at offset m(dx).
+//    Tiles of rows that do not pair with this window row, and the j = i
+//    tile, are fetched from an out-of-range coordinate: TMA zero-fills them.
+//    RB (2R + 1) tiles per row, one per thread, completing on the stage's
+//    mbarrier; NLM_NS row stages in flight.
+//  * the neighbours Z_j: the row's 9 planes over NLM_TX + 2 V3_RMAX columns
+//    (zero-filled outside the image), staged by cp.async into a ring of
+//    NLM_NZ rows; each Z_j is read from shared memory once per thread and
+//    serves its RB pairs.
+// Window rows above the owned rows are all-backward, rows below all-forward
+// (fully unrolled, branch-free); the RB rows in between mix both laws and
+// the self pair, whose w_ii = 1 is added after the row.  Columns within R of
+// the image edge mask the out-of-image pairs.  Shared-memory reads are
+// conflict-free (consecutive lanes, consecutive columns).  Per window row the
+// pairs are summed in WT (2R + 1 terms), then added to fp64 totals in a fixed
+// order per pixel: bit-reproducible, and slab decompositions are exact.
+#ifndef POLSAR_NLM_RB
+#define POLSAR_NLM_RB 4
+#endif
+#ifndef POLSAR_NLM_NS
+#define POLSAR_NLM_NS 2
+#endif
+constexpr int NLM_TX = 128;                    // threads per CTA = TMA tile length
+constexpr int NLM_NZ = 3;                      // Z row buffers
+constexpr int NLM_ZW = NLM_TX + 2 * V3_RMAX;   // staged Z columns x0 - 12 .. x0 + 139
+constexpr int NLM_OOB = -(1 << 30);            // a TMA coordinate whose tile is all zero-fill
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    int src_bytes = valid ? 4 : 0;  // 0: zero-fill
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(sa), "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+
+// stage window row gy (9 planes, columns x0 - V3_RMAX .. x0 + NLM_TX + V3_RMAX - 1)
+template <typename S>
+__device__ __forceinline__ void nlm_stage_row(S* dst, const S* __restrict__ z, int64_t ld,
+                                              int64_t width, int64_t gy, int64_t x0) {
+    const S* src = z + gy * width;
+    for (int c = threadIdx.x; c < NLM_ZW; c += NLM_TX) {
+        const int64_t gx = x0 - V3_RMAX + c;
+        const bool ok = gx >= 0 && gx < width;
+        const S* sp = src + (ok ? gx : 0);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            if constexpr (sizeof(S) == 4)
+                cp_async4(dst + k * NLM_ZW + c, sp + k * ld, ok);
+            else
+                cp_async8(dst + k * NLM_ZW + c, sp + k * ld, ok);
+        }
+    }
+}
+
+template <int AL>
+__host__ __device__ __forceinline__ int nlm_mis(int wx) { return wx & (AL - 1); }
+
+// TMA coordinate (element index in the flattened weight buffer, a multiple
+// of AL) of the tile of owned row yi at dx for window row gy.
+template <int AL>
+__device__ __forceinline__ int64_t nlm_tile_coord(int64_t gy, int64_t yi, int wx, int R, int64_t wp,
+                                                  int64_t x0, int64_t P, int64_t row_end) {
+    const int64_t dy = gy - yi;
+    if (yi >= row_end || dy < -R || dy > R || (dy == 0 && wx == 0)) return NLM_OOB;
+    const int64_t ad = dy < 0 ? -dy : dy;
+    const int64_t fi = ad == 0 ? -1 : R + (ad - 1) * (2 * R + 1) + R;  // fwd_index(|dy|, 0)
+    if (dy > 0 || (dy == 0 && wx > 0)) return (fi + wx) * P + yi * wp + x0;  // forward: at i
+    return (fi - wx) * P + gy * wp + x0 + wx - nlm_mis<AL>(wx);              // backward: at j
+}
+
+template <typename WT>
+size_t nlm_smem_bytes(int R, int RB, int NS, size_t s_bytes) {
+    return 128 + (size_t)NS * RB * (2 * R + 1) * NLM_TX * sizeof(WT) + (size_t)NLM_NZ * 9 * NLM_ZW * s_bytes;
+}
+
+// One window row for one thread: K = 0 all rows backward, 1 all forward,
+// 2 mixed (cls[r]: 0 backward, 1 forward, 2 the pixel's own row, backward for
+// dx < 0 and forward for dx > 0; its dx = 0 tile is zero); EDGE masks
+// out-of-image columns.
+#ifndef POLSAR_NLM_UNROLL
+#define POLSAR_NLM_UNROLL 4
+#endif
+constexpr int kNlmUnroll = POLSAR_NLM_UNROLL;
+template <typename WT, int AL, int RB, int K, bool EDGE, int RC>
+__device__ __forceinline__ void nlm_row(const WT* __restrict__ wrow, const WT* __restrict__ zrowT, int R,
+                                        const int (&cls)[RB], int64_t x, int64_t width, WT (&pw)[RB],
+                                        WT (&pz)[RB][9]) {
+    // wrow: w(r, dx) tile at wrow[(r * (2R + 1) + dx) * NLM_TX] (+ m(dx) for backward tiles)
+    // zrowT: Z_j(dx) at zrowT[k * NLM_ZW + dx]
+    // (a rolled loop: the per-dx body is 9 + RB loads and 10 RB FMA/adds; a
+    // fully unrolled row measured slower, instruction-fetch bound)
+    const int WX = RC > 0 ? 2 * RC + 1 : 2 * R + 1;
+    const WT* zp = zrowT - R;
+    const WT* wp = wrow - R * NLM_TX;
+#pragma unroll(kNlmUnroll)
+    for (int wx = -R; wx <= R; ++wx, ++zp, wp += NLM_TX) {
+        WT zj[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) zj[k] = zp[k * NLM_ZW];
+        const bool colok = !EDGE || (x + wx >= 0 && x + wx < width);
+        const int m = nlm_mis<AL>(wx);
+        const WT* wpm = wp + (K == 1 ? 0 : m);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            const WT* a;
+            if constexpr (K == 2)
+                a = (cls[r] == 0 || (cls[r] == 2 && wx < 0)) ? wpm : wp;
+            else
+                a = wpm;
+            WT w = a[r * WX * NLM_TX];
+            if constexpr (EDGE) w = colok ? w : WT(0);
+            pw[r] = ADD(pw[r], w);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) pz[r][k] = FMA(w, zj[k], pz[r][k]);
+        }
+    }
+}
+
+template <typename S, typename WT, int RC, int RB, int NS>
+__global__ void __launch_bounds__(NLM_TX)
+k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const S* __restrict__ z, int64_t ld,
+             int64_t width, int64_t slab_rows, int64_t row_begin, int64_t row_end, int R_rt,
+             S* __restrict__ out_w, S* __restrict__ out_z, int64_t ld_out) {
+    constexpr int AL = 16 / sizeof(WT);
+    constexpr int COLS = NLM_TX - AL;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int R = RC > 0 ? RC : R_rt;
+    const int WX = 2 * R + 1;
+    const int SW = RB * WX * NLM_TX;  // weights per stage
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    WT* wst = reinterpret_cast<WT*>(smem_raw + 128);
+    S* zs = reinterpret_cast<S*>(smem_raw + 128 + (size_t)NS * SW * sizeof(WT));
+    const CUtensorMap* pmap = &wmap;
+
+    const int64_t wp = weight_pitch<WT>(width);
+    const int64_t P = slab_rows * wp;  // weight-plane stride
+    const int64_t x0 = (int64_t)blockIdx.x * COLS;
+    const int tx = threadIdx.x;
+    const int64_t x = x0 + tx;
+    const int64_t y0 = row_begin + (int64_t)blockIdx.y * RB;
+    const bool colin = tx < COLS && x < width;  // (other threads still stage rows)
+    const bool inx = x - R >= 0 && x + R < width;
+    const int64_t ga = y0 - R > 0 ? y0 - R : 0;
+    const int64_t gb = (y0 + RB - 1 + R) < slab_rows - 1 ? (y0 + RB - 1 + R) : slab_rows - 1;
+    const int nrows = (int)(gb - ga + 1);
+
+    if (tx == 0) {
+        for (int st = 0; st < NS; ++st) mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // weights of window row q -> stage q % NS: thread t fetches tile t = (r, dx)
+    auto issue = [&](int q) {
+        const int64_t gy = ga + q;
+        const int st = q % NS;
+        if (tx == 0) mbar_expect_tx(&bar[st], (uint32_t)(SW * sizeof(WT)));
+        for (int t = tx; t < RB * WX; t += NLM_TX) {
+            const int r = t / WX, wx = t - r * WX - R;
+            const int64_t c = nlm_tile_coord<AL>(gy, y0 + r, wx, R, wp, x0, P, row_end);
+            tma_load_1d(wst + (size_t)st * SW + (size_t)t * NLM_TX, pmap, (int)c, &bar[st]);
+        }
+    };
+#pragma unroll
+    for (int q = 0; q < NS - 1; ++q)
+        if (q < nrows) issue(q);
+#pragma unroll
+    for (int q = 0; q < NLM_NZ - 1; ++q) {
+        if (q < nrows) nlm_stage_row<S>(zs + (size_t)q * 9 * NLM_ZW, z, ld, width, ga + q, x0);
+        cp_async_commit();
+    }
+
+    double tw[RB], tz[RB][9];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        tw[r] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) tz[r][k] = 0.0;
+    }
+    for (int q = 0; q < nrows; ++q) {
+        const int64_t gy = ga + q;
+        // refill the stage and ring slot row q - 1 used (released by the barrier that ended it)
+        if (q + NS - 1 < nrows) issue(q + NS - 1);
+        if (q + NLM_NZ - 1 < nrows)
+            nlm_stage_row<S>(zs + (size_t)((q + NLM_NZ - 1) % NLM_NZ) * 9 * NLM_ZW, z, ld, width,
+                             gy + NLM_NZ - 1, x0);
+        cp_async_commit();
+        cp_async_wait<NLM_NZ - 1>();
+        __syncthreads();
+        mbar_wait(&bar[q % NS], (uint32_t)((q / NS) & 1));
+        if (colin) {
+            const S* zrow = zs + (size_t)(q % NLM_NZ) * 9 * NLM_ZW + tx + V3_RMAX;
+            const WT* wrow = wst + (size_t)(q % NS) * SW + tx + R * NLM_TX;
+            WT pw[RB], pz[RB][9];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                pw[r] = WT(0);
+#pragma unroll
+                for (int k = 0; k < 9; ++k) pz[r][k] = WT(0);
+            }
+            int cls[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) cls[r] = gy < y0 + r ? 0 : (gy > y0 + r ? 1 : 2);
+            const int K = gy < y0 ? 0 : (gy >= y0 + RB ? 1 : 2);  // CTA-uniform
+            static_assert(sizeof(S) == sizeof(WT), "the gather reads Z in the weight type");
+            const WT* zr = reinterpret_cast<const WT*>(zrow);
+            if (inx) {
+                if (K == 0) nlm_row<WT, AL, RB, 0, false, RC>(wrow, zr, R, cls, x, width, pw, pz);
+                else if (K == 1) nlm_row<WT, AL, RB, 1, false, RC>(wrow, zr, R, cls, x, width, pw, pz);
+                else nlm_row<WT, AL, RB, 2, false, RC>(wrow, zr, R, cls, x, width, pw, pz);
+            } else {
+                if (K == 0) nlm_row<WT, AL, RB, 0, true, RC>(wrow, zr, R, cls, x, width, pw, pz);
+                else if (K == 1) nlm_row<WT, AL, RB, 1, true, RC>(wrow, zr, R, cls, x, width, pw, pz);
+                else nlm_row<WT, AL, RB, 2, true, RC>(wrow, zr, R, cls, x, width, pw, pz);
+            }
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                if (gy == y0 + r && y0 + r < row_end) {  // the self pair: w_ii = 1 (d_ii = 0)
+                    pw[r] = ADD(pw[r], WT(1));
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) pz[r][k] = ADD(pz[r][k], zr[k * NLM_ZW]);
+                }
+                tw[r] = __dadd_rn(tw[r], (double)pw[r]);
+#pragma unroll
+                for (int k = 0; k < 9; ++k) tz[r][k] = __dadd_rn(tz[r][k], (double)pz[r][k]);
+            }
+        }
+        __syncthreads();  // stage q % NS and ring slot q % NLM_NZ are refilled from row q + 1
+    }
+    if (!colin) return;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        const int64_t yi = y0 + r;
+        if (yi < row_end) {
+            const int64_t o = (yi - row_begin) * width + x;
+            if (out_w) out_w[o] = (S)tw[r];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) out_z[k * ld_out + o] = (S)__ddiv_rn(tz[r][k], tw[r]);
+        }
+    }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// 1-D tiled tensor map over the weight planes (fwd_count(R) * N elements),
+// box NLM_TX; false if the driver call is unavailable or refuses.
+template <typename WT>
+bool nlm_weight_map(CUtensorMap* m, const WT* wbuf, int64_t total) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dim[1] = {(cuuint64_t)total};
+    // (rank 1 has no strides, but the driver rejects a null array: measured,
+    // tools/micro/tmap_probe.cu)
+    cuuint64_t st[1] = {(cuuint64_t)total * sizeof(WT)};
+    cuuint32_t box[1] = {(cuuint32_t)NLM_TX};
+    cuuint32_t es[1] = {1};
+    CUresult r = enc(m, sizeof(WT) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1,
+                     (void*)wbuf, dim, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <typename S, typename T, typename WT>
+int launch_nlm_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
+                   int64_t re, int R, double looks, double h, void* wsv, void* out_w, void* out_z,
+                   int64_t ld_out, cudaStream_t s) {
+    const S* z = (const S*)zv;
+    const int64_t n = slab_rows * width;
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    unsigned char* ws = (unsigned char*)wsv;
+    WT* g = (WT*)ws;
+    double* fbuf = (double*)(ws + up(n * sizeof(WT)));
+    WT* wbuf = (WT*)(ws + up(n * sizeof(WT)) + up(n * sizeof(double)));
+    constexpr int RB = sizeof(WT) == 4 ? POLSAR_NLM_RB : 2;
+    constexpr int NS = POLSAR_NLM_NS;
+    CUtensorMap wmap;
+    if (!nlm_weight_map<WT>(&wmap, wbuf, (int64_t)fwd_count(R) * slab_rows * weight_pitch<WT>(width)))
+        return fail(POLSAR_ECUDA, "polsar_nlm_filter: cuTensorMapEncodeTiled failed");
+    const size_t smem = nlm_smem_bytes<WT>(R, RB, NS, sizeof(S));
+    auto kern = R == 11 ? k_nlm_gather<S, WT, 11, RB, NS> : k_nlm_gather<S, WT, 0, RB, NS>;
+    if (smem > K3_SMEM_MAX ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return fail(POLSAR_ENOTSUP, "polsar_nlm_filter: shared memory request too large");
+    k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
+    const double alpha = looks / (2.0 * h);
+    LogDetPair<S, T, WT> pr{z, ld, g, (WT)alpha, alpha == 2.0};
+    int rc = launch_fwd<LogDetPair<S, T, WT>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
+        pr, width, slab_rows, rb, re, R, wbuf, fbuf, s,
+        "polsar_nlm_filter: shared memory request too large");
+    if (rc != POLSAR_OK) return rc;
+    constexpr int COLS = NLM_TX - 16 / (int)sizeof(WT);
+    dim3 grid((unsigned)((width + COLS - 1) / COLS), (unsigned)((re - rb + RB - 1) / RB));
+    kern<<<grid, NLM_TX, smem, s>>>(wmap, z, ld, width, slab_rows, rb, re, R, (S*)out_w, (S*)out_z, ld_out);
+    return launch_check("polsar_nlm_filter: launch failed");
+}
+
+// NLM variant: symmetric (pass 1 + gather, default for R <= V3_RMAX) or the
+// direct form (POLSAR_NLM_VARIANT=direct, and always for R > V3_RMAX).
+bool nlm_direct() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("POLSAR_NLM_VARIANT");
+        v = (e && e[0] == 'd') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 }  // namespace
 }  // namespace polsar_impl
 
@@ -1254,9 +1616,11 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radiu
     size_t b = (((size_t)n * (wt64 ? 8 : 4)) + 255) / 256 * 256;
     if (dtype != POLSAR_F32_PLAIN) b = std::max(b, ((size_t)n * 160 + 255) / 256 * 256);
     if (radius <= V3_RMAX) {
-        b = std::max(b, wt64 ? window_sym_bytes<double>(n, radius) : window_sym_bytes<float>(n, radius));
+        b = std::max(b, wt64 ? window_sym_bytes<double>(slab_rows, width, radius)
+                             : window_sym_bytes<float>(slab_rows, width, radius));
         if (dtype != POLSAR_F32_PLAIN)
-            b = std::max(b, wt64 ? kl_sym_bytes<double>(n, radius) : kl_sym_bytes<float>(n, radius));
+            b = std::max(b, wt64 ? kl_sym_bytes<double>(slab_rows, width, radius)
+                                 : kl_sym_bytes<float>(slab_rows, width, radius));
     }
     return b;
 }
@@ -1351,6 +1715,26 @@ int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_row
     if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
     if (!z || !workspace || !out_z) return fail(POLSAR_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)cuda_stream;
+    // (the symmetric form's gather addresses the weight buffer with 32-bit TMA coordinates)
+    if (radius >= 1 && radius <= V3_RMAX && !nlm_direct() && tensor_map_encoder() &&
+        (int64_t)fwd_count(radius) * slab_rows * (width + 4) + NLM_TX < ((int64_t)1 << 31) - 1) {
+        switch (dtype) {
+            case POLSAR_F32:
+                return launch_nlm_sym<float, double, float>(z, ld, width, slab_rows, out_row_begin,
+                                                            out_row_end, radius, looks, h, workspace,
+                                                            out_w, out_z, ld_out, s);
+            case POLSAR_F64:
+            case POLSAR_F64_PLAIN:
+                return launch_nlm_sym<double, double, double>(z, ld, width, slab_rows, out_row_begin,
+                                                              out_row_end, radius, looks, h, workspace,
+                                                              out_w, out_z, ld_out, s);
+            case POLSAR_F32_PLAIN:
+                return launch_nlm_sym<float, float, float>(z, ld, width, slab_rows, out_row_begin,
+                                                           out_row_end, radius, looks, h, workspace,
+                                                           out_w, out_z, ld_out, s);
+            default: return fail(POLSAR_EINVAL, "bad dtype");
+        }
+    }
     switch (dtype) {
         case POLSAR_F32:
             return launch_nlm<float, double, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,

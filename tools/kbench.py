@@ -33,6 +33,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--what", default="window,k1")
     ap.add_argument("--rows", type=int, default=2500)
+    ap.add_argument("--ref", default="", help="nlm: save outputs here, or compare with them")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     s = torch.cuda.Stream()
@@ -67,6 +68,21 @@ def main():
             res["window_c5_fp64_ms"] = timeit(lambda: P.polsar_window_distance(
                 z64, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, out,
                 stream=s), s, steps=3)
+        if a.what == "nlm":
+            c5 = configs.get("c5")
+            z = wishart.generate(c5, device=dev, stream=s)
+            zz = torch.empty((9, c5.n), dtype=z.dtype, device=dev)
+            wo = torch.empty(c5.n, dtype=z.dtype, device=dev)
+            ws32 = torch.empty(P.polsar_window_workspace_bytes(c5.height, c5.width, c5.radius, 0),
+                               dtype=torch.uint8, device=dev)
+            res["nlm_c5_ms"] = timeit(lambda: P.polsar_nlm_filter(z, c5.width, c5.height, 0, c5.height,
+                                                                  c5.radius, c5.looks, c5.h, ws32, zz, wo,
+                                                                  stream=s), s, steps=5)
+            ref = torch.load(a.ref) if a.ref and os.path.exists(a.ref) else None
+            if a.ref and ref is None:
+                torch.save({"z": zz.cpu(), "w": wo.cpu()}, a.ref)
+            elif ref is not None:
+                res["nlm_bit_identical_to_ref"] = bool(torch.equal(ref["z"], zz.cpu()) and torch.equal(ref["w"], wo.cpu()))
         if "k1" in a.what:
             c3 = configs.get("c3").scaled(a.rows)
             z = wishart.generate(c3, device=dev, stream=s)
