@@ -1297,7 +1297,7 @@ int launch_window_kl_sym(const void* zv, int64_t ld, int64_t width, int64_t slab
 // pairs are summed in WT (2R + 1 terms), then added to fp64 totals in a fixed
 // order per pixel: bit-reproducible, and slab decompositions are exact.
 #ifndef POLSAR_NLM_RB
-#define POLSAR_NLM_RB 4
+#define POLSAR_NLM_RB 2
 #endif
 #ifndef POLSAR_NLM_NS
 #define POLSAR_NLM_NS 2
@@ -1305,6 +1305,13 @@ int launch_window_kl_sym(const void* zv, int64_t ld, int64_t width, int64_t slab
 constexpr int NLM_TX = 128;                    // threads per CTA = TMA tile length
 constexpr int NLM_NZ = 3;                      // Z row buffers
 constexpr int NLM_ZW = NLM_TX + 2 * V3_RMAX;   // staged Z columns x0 - 12 .. x0 + 139
+// Z record of one staged column: the 9 planes padded to 16-byte vectors
+// (12 floats / 10 doubles; strides of 12 and 20 words keep the 16-byte
+// loads of 8 consecutive lanes on distinct banks)
+template <typename S>
+struct NlmRec {
+    static constexpr int n = sizeof(S) == 4 ? 12 : 10;
+};
 constexpr int NLM_OOB = -(1 << 30);            // a TMA coordinate whose tile is all zero-fill
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
@@ -1319,6 +1326,7 @@ template <typename S>
 __device__ __forceinline__ void nlm_stage_row(S* dst, const S* __restrict__ z, int64_t ld,
                                               int64_t width, int64_t gy, int64_t x0) {
     const S* src = z + gy * width;
+    constexpr int ZR = NlmRec<S>::n;
     for (int c = threadIdx.x; c < NLM_ZW; c += NLM_TX) {
         const int64_t gx = x0 - V3_RMAX + c;
         const bool ok = gx >= 0 && gx < width;
@@ -1326,9 +1334,9 @@ __device__ __forceinline__ void nlm_stage_row(S* dst, const S* __restrict__ z, i
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
             if constexpr (sizeof(S) == 4)
-                cp_async4(dst + k * NLM_ZW + c, sp + k * ld, ok);
+                cp_async4(dst + c * ZR + k, sp + k * ld, ok);
             else
-                cp_async8(dst + k * NLM_ZW + c, sp + k * ld, ok);
+                cp_async8(dst + c * ZR + k, sp + k * ld, ok);
         }
     }
 }
@@ -1351,13 +1359,31 @@ __device__ __forceinline__ int64_t nlm_tile_coord(int64_t gy, int64_t yi, int wx
 
 template <typename WT>
 size_t nlm_smem_bytes(int R, int RB, int NS, size_t s_bytes) {
-    return 128 + (size_t)NS * RB * (2 * R + 1) * NLM_TX * sizeof(WT) + (size_t)NLM_NZ * 9 * NLM_ZW * s_bytes;
+    return 128 + (size_t)NS * RB * (2 * R + 1) * NLM_TX * sizeof(WT) +
+           (size_t)NLM_NZ * NLM_ZW * (s_bytes == 4 ? 12 : 10) * s_bytes;
 }
 
 // One window row for one thread: K = 0 all rows backward, 1 all forward,
 // 2 mixed (cls[r]: 0 backward, 1 forward, 2 the pixel's own row, backward for
 // dx < 0 and forward for dx > 0; its dx = 0 tile is zero); EDGE masks
 // out-of-image columns.
+__device__ __forceinline__ void nlm_load_rec(const float* p, float (&zj)[9]) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0];
+    const float4 b = reinterpret_cast<const float4*>(p)[1];
+    zj[0] = a.x; zj[1] = a.y; zj[2] = a.z; zj[3] = a.w;
+    zj[4] = b.x; zj[5] = b.y; zj[6] = b.z; zj[7] = b.w;
+    zj[8] = p[8];
+}
+__device__ __forceinline__ void nlm_load_rec(const double* p, double (&zj)[9]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double2 v = reinterpret_cast<const double2*>(p)[k];
+        zj[2 * k] = v.x;
+        zj[2 * k + 1] = v.y;
+    }
+    zj[8] = p[8];
+}
+
 #ifndef POLSAR_NLM_UNROLL
 #define POLSAR_NLM_UNROLL 4
 #endif
@@ -1367,17 +1393,17 @@ __device__ __forceinline__ void nlm_row(const WT* __restrict__ wrow, const WT* _
                                         const int (&cls)[RB], int64_t x, int64_t width, WT (&pw)[RB],
                                         WT (&pz)[RB][9]) {
     // wrow: w(r, dx) tile at wrow[(r * (2R + 1) + dx) * NLM_TX] (+ m(dx) for backward tiles)
-    // zrowT: Z_j(dx) at zrowT[k * NLM_ZW + dx]
+    // zrowT: the record of Z_j(dx) at zrowT + dx * ZR
     // (a rolled loop: the per-dx body is 9 + RB loads and 10 RB FMA/adds; a
     // fully unrolled row measured slower, instruction-fetch bound)
     const int WX = RC > 0 ? 2 * RC + 1 : 2 * R + 1;
-    const WT* zp = zrowT - R;
+    constexpr int ZR = NlmRec<WT>::n;
+    const WT* zp = zrowT - R * ZR;
     const WT* wp = wrow - R * NLM_TX;
 #pragma unroll(kNlmUnroll)
-    for (int wx = -R; wx <= R; ++wx, ++zp, wp += NLM_TX) {
+    for (int wx = -R; wx <= R; ++wx, zp += ZR, wp += NLM_TX) {
         WT zj[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) zj[k] = zp[k * NLM_ZW];
+        nlm_load_rec(zp, zj);
         const bool colok = !EDGE || (x + wx >= 0 && x + wx < width);
         const int m = nlm_mis<AL>(wx);
         const WT* wpm = wp + (K == 1 ? 0 : m);
@@ -1399,7 +1425,8 @@ __device__ __forceinline__ void nlm_row(const WT* __restrict__ wrow, const WT* _
 
 template <typename S, typename WT, int RC, int RB, int NS>
 __global__ void __launch_bounds__(NLM_TX)
-k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const S* __restrict__ z, int64_t ld,
+k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap wmap2,
+             const S* __restrict__ z, int64_t ld,
              int64_t width, int64_t slab_rows, int64_t row_begin, int64_t row_end, int R_rt,
              S* __restrict__ out_w, S* __restrict__ out_z, int64_t ld_out) {
     constexpr int AL = 16 / sizeof(WT);
@@ -1412,6 +1439,8 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const S* __restrict__ z, 
     WT* wst = reinterpret_cast<WT*>(smem_raw + 128);
     S* zs = reinterpret_cast<S*>(smem_raw + 128 + (size_t)NS * SW * sizeof(WT));
     const CUtensorMap* pmap = &wmap;
+    const CUtensorMap* pmap2 = &wmap2;
+    constexpr int ZREC = NLM_ZW * NlmRec<S>::n;  // one staged row
 
     const int64_t wp = weight_pitch<WT>(width);
     const int64_t P = slab_rows * wp;  // weight-plane stride
@@ -1437,8 +1466,20 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const S* __restrict__ z, 
         if (tx == 0) mbar_expect_tx(&bar[st], (uint32_t)(SW * sizeof(WT)));
         for (int t = tx; t < RB * WX; t += NLM_TX) {
             const int r = t / WX, wx = t - r * WX - R;
-            const int64_t c = nlm_tile_coord<AL>(gy, y0 + r, wx, R, wp, x0, P, row_end);
-            tma_load_1d(wst + (size_t)st * SW + (size_t)t * NLM_TX, pmap, (int)c, &bar[st]);
+            const int64_t yi = y0 + r, dy = gy - yi;
+            if (yi >= row_end || dy < -R || dy > R || dy > 0) {
+                // a whole forward row (the 2R + 1 planes fwd_index(dy, -R..R) at i: one
+                // 2-D box), or a row that does not pair (one out-of-range box: zeros)
+                if (wx == -R) {
+                    const bool act = yi < row_end && dy >= -R && dy <= R;
+                    const int c0 = act ? (int)(yi * wp + x0) : 0;
+                    const int c1 = act ? R + (int)(dy - 1) * (2 * R + 1) : NLM_OOB;
+                    tma_load_2d(wst + (size_t)st * SW + (size_t)t * NLM_TX, pmap2, c0, c1, &bar[st]);
+                }
+            } else {
+                const int64_t c = nlm_tile_coord<AL>(gy, yi, wx, R, wp, x0, P, row_end);
+                tma_load_1d(wst + (size_t)st * SW + (size_t)t * NLM_TX, pmap, (int)c, &bar[st]);
+            }
         }
     };
 #pragma unroll
@@ -1446,7 +1487,7 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const S* __restrict__ z, 
         if (q < nrows) issue(q);
 #pragma unroll
     for (int q = 0; q < NLM_NZ - 1; ++q) {
-        if (q < nrows) nlm_stage_row<S>(zs + (size_t)q * 9 * NLM_ZW, z, ld, width, ga + q, x0);
+        if (q < nrows) nlm_stage_row<S>(zs + (size_t)q * ZREC, z, ld, width, ga + q, x0);
         cp_async_commit();
     }
 
@@ -1462,14 +1503,14 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const S* __restrict__ z, 
         // refill the stage and ring slot row q - 1 used (released by the barrier that ended it)
         if (q + NS - 1 < nrows) issue(q + NS - 1);
         if (q + NLM_NZ - 1 < nrows)
-            nlm_stage_row<S>(zs + (size_t)((q + NLM_NZ - 1) % NLM_NZ) * 9 * NLM_ZW, z, ld, width,
+            nlm_stage_row<S>(zs + (size_t)((q + NLM_NZ - 1) % NLM_NZ) * ZREC, z, ld, width,
                              gy + NLM_NZ - 1, x0);
         cp_async_commit();
         cp_async_wait<NLM_NZ - 1>();
         __syncthreads();
         mbar_wait(&bar[q % NS], (uint32_t)((q / NS) & 1));
         if (colin) {
-            const S* zrow = zs + (size_t)(q % NLM_NZ) * 9 * NLM_ZW + tx + V3_RMAX;
+            const S* zrow = zs + (size_t)(q % NLM_NZ) * ZREC + (tx + V3_RMAX) * NlmRec<S>::n;
             const WT* wrow = wst + (size_t)(q % NS) * SW + tx + R * NLM_TX;
             WT pw[RB], pz[RB][9];
 #pragma unroll
@@ -1498,7 +1539,7 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const S* __restrict__ z, 
                 if (gy == y0 + r && y0 + r < row_end) {  // the self pair: w_ii = 1 (d_ii = 0)
                     pw[r] = ADD(pw[r], WT(1));
 #pragma unroll
-                    for (int k = 0; k < 9; ++k) pz[r][k] = ADD(pz[r][k], zr[k * NLM_ZW]);
+                    for (int k = 0; k < 9; ++k) pz[r][k] = ADD(pz[r][k], zr[k]);
                 }
                 tw[r] = __dadd_rn(tw[r], (double)pw[r]);
 #pragma unroll
@@ -1554,6 +1595,23 @@ bool nlm_weight_map(CUtensorMap* m, const WT* wbuf, int64_t total) {
     return r == CUDA_SUCCESS;
 }
 
+// 2-D view (P x planes, row stride P) with a box of NLM_TX x rows: a forward
+// row's 2R + 1 consecutive planes in one transfer
+template <typename WT>
+bool nlm_weight_map2(CUtensorMap* m, const WT* wbuf, int64_t P, int planes, int rows) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dim[2] = {(cuuint64_t)P, (cuuint64_t)planes};
+    cuuint64_t st[1] = {(cuuint64_t)P * sizeof(WT)};
+    cuuint32_t box[2] = {(cuuint32_t)NLM_TX, (cuuint32_t)rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, sizeof(WT) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                     (void*)wbuf, dim, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <typename S, typename T, typename WT>
 int launch_nlm_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
                    int64_t re, int R, double looks, double h, void* wsv, void* out_w, void* out_z,
@@ -1567,8 +1625,10 @@ int launch_nlm_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows,
     WT* wbuf = (WT*)(ws + up(n * sizeof(WT)) + up(n * sizeof(double)));
     constexpr int RB = sizeof(WT) == 4 ? POLSAR_NLM_RB : 2;
     constexpr int NS = POLSAR_NLM_NS;
-    CUtensorMap wmap;
-    if (!nlm_weight_map<WT>(&wmap, wbuf, (int64_t)fwd_count(R) * slab_rows * weight_pitch<WT>(width)))
+    CUtensorMap wmap, wmap2;
+    const int64_t P = slab_rows * weight_pitch<WT>(width);
+    if (!nlm_weight_map<WT>(&wmap, wbuf, (int64_t)fwd_count(R) * P) ||
+        !nlm_weight_map2<WT>(&wmap2, wbuf, P, fwd_count(R), 2 * R + 1))
         return fail(POLSAR_ECUDA, "polsar_nlm_filter: cuTensorMapEncodeTiled failed");
     const size_t smem = nlm_smem_bytes<WT>(R, RB, NS, sizeof(S));
     auto kern = R == 11 ? k_nlm_gather<S, WT, 11, RB, NS> : k_nlm_gather<S, WT, 0, RB, NS>;
@@ -1584,7 +1644,7 @@ int launch_nlm_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows,
     if (rc != POLSAR_OK) return rc;
     constexpr int COLS = NLM_TX - 16 / (int)sizeof(WT);
     dim3 grid((unsigned)((width + COLS - 1) / COLS), (unsigned)((re - rb + RB - 1) / RB));
-    kern<<<grid, NLM_TX, smem, s>>>(wmap, z, ld, width, slab_rows, rb, re, R, (S*)out_w, (S*)out_z, ld_out);
+    kern<<<grid, NLM_TX, smem, s>>>(wmap, wmap2, z, ld, width, slab_rows, rb, re, R, (S*)out_w, (S*)out_z, ld_out);
     return launch_check("polsar_nlm_filter: launch failed");
 }
 
