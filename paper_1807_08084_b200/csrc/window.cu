@@ -1510,6 +1510,8 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ C
         __syncthreads();
         mbar_wait(&bar[q % NS], (uint32_t)((q / NS) & 1));
         if (colin) {
+            // records dx = -R..R of column tx, and tile elements tx + m(dx) (m < AL)
+            POLSAR_CHECK(tx + V3_RMAX - R >= 0 && tx + V3_RMAX + R < NLM_ZW && tx + AL - 1 < NLM_TX);
             const S* zrow = zs + (size_t)(q % NLM_NZ) * ZREC + (tx + V3_RMAX) * NlmRec<S>::n;
             const WT* wrow = wst + (size_t)(q % NS) * SW + tx + R * NLM_TX;
             WT pw[RB], pz[RB][9];

@@ -17,8 +17,12 @@ THREADS = len(os.sched_getaffinity(0))
 TOL = {torch.float32: 2e-5, torch.float64: 4e-10}
 
 
+# shapes cover the symmetric form's gather (R <= 12: several 124-column CTA
+# strips, widths not a multiple of 4, one row, a narrow image, R = 12) and the
+# direct form (R = 0, R > 12)
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
-@pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 53), 3), ((40, 45), 14)])
+@pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 53), 3), ((40, 45), 14), ((20, 70), 0),
+                                          ((5, 300), 12), ((130, 7), 1), ((1, 50), 4), ((60, 250), 11)])
 def test_nlm_parity(cuda, dt, shape, radius):
     h, w = shape
     z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda).to(dt)
@@ -75,3 +79,53 @@ def test_nlm_c5_full_size_sampled(cuda):
     err = np.max(np.abs(got - rz), axis=0) / np.max(np.abs(rz), axis=0)
     assert err.max() <= 2e-5
     assert (np.abs(W[ii].cpu().numpy() - rw) / rw).max() <= 2e-5
+
+
+@pytest.mark.parametrize("looks,hh", [(3.0, 1.0), (8.0, 2.0)])
+def test_nlm_general_exponent(cuda, looks, hh):
+    """alpha = L / (2h) != 2: the weight through MUFU lg2 / ex2 in pass 1."""
+    h, w, r = 40, 45, 5
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda)
+    zhat, W = P.nlm_filter(z, h, w, radius=r, looks=looks, h=hh)
+    rz, rw = oracle.nlm_threaded(z.cpu().numpy(), h, w, r, looks, hh, np.arange(h * w), THREADS)
+    err = np.max(np.abs(zhat.cpu().numpy().astype(np.float64) - rz), axis=0) / np.max(np.abs(rz), axis=0)
+    assert err.max() <= 2e-5
+    assert (np.abs(W.cpu().numpy() - rw) / rw).max() <= 2e-5
+
+
+def test_nlm_plain_mode(cuda):
+    """POLSAR_F32_PLAIN (fp32 pair determinant): reported, not held to 2e-5;
+    it must still be a valid weighted mean (W in [1, |N(i)|], Zhat finite)."""
+    h, w, r = 64, 64, 11
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda)
+    zhat, W = P.nlm_filter(z, h, w, radius=r, plain=True)
+    assert torch.isfinite(zhat).all()
+    assert (W >= 1 - 1e-6).all() and (W <= (2 * r + 1) ** 2 + 1e-3).all()
+    rz, rw = oracle.nlm_threaded(z.cpu().numpy(), h, w, r, 4.0, 1.0, np.arange(h * w), THREADS)
+    assert (np.abs(W.cpu().numpy() - rw) / rw).max() <= 1e-3
+
+
+def test_nlm_direct_variant_subprocess(cuda):
+    """POLSAR_NLM_VARIANT=direct (read once per process): the direct form
+    against the oracle in a child process, on the same inputs as the default."""
+    import subprocess
+    import sys
+    code = r'''
+import os, numpy as np, torch, oracle
+import paper_1807_08084_b200 as P
+from paper_1807_08084_b200 import configs, wishart
+dev = torch.device("cuda:0")
+h, w, r = 60, 250, 11
+z = wishart.generate(configs.get("c5").scaled(h, w), device=dev)
+zhat, W = P.nlm_filter(z, h, w, radius=r)
+rz, rw = oracle.nlm_threaded(z.cpu().numpy(), h, w, r, 4.0, 1.0, np.arange(h * w), len(os.sched_getaffinity(0)))
+err = np.max(np.abs(zhat.cpu().numpy().astype(np.float64) - rz), axis=0) / np.max(np.abs(rz), axis=0)
+assert err.max() <= 2e-5, err.max()
+assert (np.abs(W.cpu().numpy() - rw) / rw).max() <= 2e-5
+print("ok")
+'''
+    env = dict(os.environ, POLSAR_NLM_VARIANT="direct")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=300)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stdout + res.stderr
