@@ -868,8 +868,10 @@ constexpr int kSymUnroll = POLSAR_SYM_UNROLL;
 //
 // Log-det distance (R-12): 9 planes + g = 1/(8 det Z); w from Eq. 6 on
 // S = Z_i + Z_j (pair_w).
-template <typename S_, typename T_, typename WT_>
+template <typename S_, typename T_, typename WT_, int A2_ = -1>
 struct LogDetPair {
+    // A2_: 1 / 0 fix "alpha == 2" at compile time (the weight is 1/r^2, or
+    // MUFU lg2/ex2); -1 reads the runtime flag a2
     using S = S_;
     using T = T_;
     using WT = WT_;
@@ -903,7 +905,7 @@ struct LogDetPair {
     __device__ __forceinline__ WT post(Q ds, const Rec& i, Aux gj) const {
         WT fds = (WT)ds;
         WT rr = (fds * i.g) * (fds * gj);
-        return pair_weight(rr, alpha, a2);
+        return pair_weight(rr, alpha, A2_ < 0 ? a2 : A2_ == 1);
     }
     __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
         return post(pre(i, j), i, aux(j));
@@ -962,24 +964,31 @@ struct KLPair {
 // Pass 1, one full window row (all 2R+1 neighbours valid for every owned
 // row): weights into row[] and, for owned in-image pairs, into the planes
 // wp[r] (advanced by one plane per neighbour).
-template <typename Pair, int RB>
+template <typename Pair, int RB, bool FULL>
 __device__ __forceinline__ void fwd_full_row(const Pair& pr, const typename Pair::Rec (&ri)[RB],
                                              const typename Pair::T* rec, int R, int64_t gx,
                                              int64_t width, bool interior_x, const bool (&own)[RB],
                                              typename Pair::WT* (&wp)[RB], int64_t N,
                                              typename Pair::WT (&row)[RB]) {
+    // FULL: the CTA's whole tile is inside the image and the output rows, so
+    // every pair is in-image and owned: no masks, unconditional stores
     using WT = typename Pair::WT;
 #pragma unroll kSymUnroll
     for (int wx = -R; wx <= R; ++wx, rec += Pair::RS) {
         typename Pair::Rec rj;
         Pair::load(rec, rj);
-        const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+        const bool colok = FULL || interior_x || (gx + wx >= 0 && gx + wx < width);
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
             WT w = pr.weight(ri[r], rj);
-            w = colok ? w : WT(0);
-            row[r] += w;
-            if (colok && own[r]) *wp[r] = w;
+            if constexpr (FULL) {
+                row[r] += w;
+                *wp[r] = w;
+            } else {
+                w = colok ? w : WT(0);
+                row[r] += w;
+                if (colok && own[r]) *wp[r] = w;
+            }
             wp[r] += N;
         }
     }
@@ -1074,6 +1083,7 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
         acc[r] = 0.0;
     }
     const bool interior_x = (x0 - R >= 0) && (x0 + K3_TX + R <= width);
+    const bool full = interior_x && y0 + TY <= row_end;  // CTA-uniform
 
     for (int wy = 0; wy <= R + RB - 1; ++wy) {
         const int64_t gyj = y0 + ty0 + wy;
@@ -1092,8 +1102,10 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
             POLSAR_CHECK(hy >= 0 && hy < HH && tx + 2 * R < HW);  // records wx = -R..R
             if constexpr (Pair::kPipeline)
                 fwd_full_row_pipelined<Pair, RB>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row);
+            else if (full)
+                fwd_full_row<Pair, RB, true>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row);
             else
-                fwd_full_row<Pair, RB>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row);
+                fwd_full_row<Pair, RB, false>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row);
         } else {
             for (int wx = -R; wx <= R; ++wx, rec += RS) {
                 POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
@@ -1216,10 +1228,13 @@ int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_ro
     WT* wbuf = (WT*)(ws + up(n * sizeof(WT)) + up(n * sizeof(double)));
     k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
     const double alpha = looks / (2.0 * h);
-    LogDetPair<S, T, WT> pr{z, ld, g, (WT)alpha, alpha == 2.0};
-    int rc = launch_fwd<LogDetPair<S, T, WT>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
-        pr, width, slab_rows, rb, re, R, wbuf, fbuf, s,
-        "polsar_window_distance: shared memory request too large");
+    int rc = alpha == 2.0
+                 ? launch_fwd<LogDetPair<S, T, WT, 1>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
+                       LogDetPair<S, T, WT, 1>{z, ld, g, (WT)alpha, true}, width, slab_rows, rb, re, R,
+                       wbuf, fbuf, s, "polsar_window_distance: shared memory request too large")
+                 : launch_fwd<LogDetPair<S, T, WT, 0>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
+                       LogDetPair<S, T, WT, 0>{z, ld, g, (WT)alpha, false}, width, slab_rows, rb, re, R,
+                       wbuf, fbuf, s, "polsar_window_distance: shared memory request too large");
     if (rc != POLSAR_OK) return rc;
     launch_bwd<S, WT>(wbuf, fbuf, width, slab_rows, rb, re, R, outv, s);
     return launch_check("polsar_window_distance: launch failed");
@@ -1639,10 +1654,13 @@ int launch_nlm_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows,
         return fail(POLSAR_ENOTSUP, "polsar_nlm_filter: shared memory request too large");
     k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
     const double alpha = looks / (2.0 * h);
-    LogDetPair<S, T, WT> pr{z, ld, g, (WT)alpha, alpha == 2.0};
-    int rc = launch_fwd<LogDetPair<S, T, WT>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
-        pr, width, slab_rows, rb, re, R, wbuf, fbuf, s,
-        "polsar_nlm_filter: shared memory request too large");
+    int rc = alpha == 2.0
+                 ? launch_fwd<LogDetPair<S, T, WT, 1>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
+                       LogDetPair<S, T, WT, 1>{z, ld, g, (WT)alpha, true}, width, slab_rows, rb, re, R,
+                       wbuf, fbuf, s, "polsar_nlm_filter: shared memory request too large")
+                 : launch_fwd<LogDetPair<S, T, WT, 0>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
+                       LogDetPair<S, T, WT, 0>{z, ld, g, (WT)alpha, false}, width, slab_rows, rb, re, R,
+                       wbuf, fbuf, s, "polsar_nlm_filter: shared memory request too large");
     if (rc != POLSAR_OK) return rc;
     constexpr int COLS = NLM_TX - 16 / (int)sizeof(WT);
     dim3 grid((unsigned)((width + COLS - 1) / COLS), (unsigned)((re - rb + RB - 1) / RB));
