@@ -584,12 +584,23 @@ def run_window(args):
     pairs_rank = window_pairs_rows(H, W, R, r0, r1)
     pairs = pairs_rank * world
     ops = FP64_OPS_PER_PAIR[args.kernel]
-    variant = os.environ.get("POLSAR_WINDOW_VARIANT", "4") if args.kernel == "window" else "direct"
-    if args.kernel == "window" and variant == "4":
-        # d(i, j) is symmetric: the algorithmic work is one evaluation per
-        # unordered pair, which is what the symmetric kernel does
+    # which form the library runs (read once per process, as the library does)
+    if args.kernel == "nlm":
+        symmetric = not os.environ.get("POLSAR_NLM_VARIANT", "").startswith("d") and R <= 12
+        variant = "symmetric two-pass (pass 1 + TMA gather)" if symmetric else "direct"
+    else:
+        v = os.environ.get("POLSAR_WINDOW_VARIANT", "4")
+        symmetric = v not in ("2", "3") and R <= 12
+        variant = "symmetric two-pass" if symmetric else {"3": "det expansion", "2": "direct"}.get(v, v)
+        if args.kernel == "kl" and not symmetric:
+            variant = "streaming expansion"
+    if symmetric:
+        # d(i, j) is symmetric: the algorithmic FP64 work is one evaluation per
+        # unordered pair, which is what the symmetric kernels do;
+        # NLM's gather pass adds no FP64 work (9 FP32 FMAs per ordered pair)
         work_pairs = unordered_pairs_rows(H, W, R, r0, r1)
-        launches = 3  # prep, forward pass, backward pass
+        ops = FP64_OPS_PER_PAIR["window"] if args.kernel == "nlm" else ops
+        launches = 3  # prep, forward pass, backward / gather pass
     else:
         work_pairs = pairs_rank
         launches = 2  # prep, window sum
@@ -603,8 +614,7 @@ def run_window(args):
                                f"R={R} per GPU", "kernel": args.kernel, "halo": args.halo,
                    "l2": "compute-bound; inputs 151 MB staged once per tile",
                    "parallelism": f"dp{world} (pixel rows + {R}-row halos)",
-                   "variant": {"4": "symmetric two-pass", "3": "det expansion", "2": "direct"}.get(variant, variant)
-                   if args.kernel == "window" else "direct"},
+                   "variant": variant},
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": FP64_PEAK_OPS / 1e12,
                      "unit": "T fp64-ops/s", "frac": achieved / FP64_PEAK_OPS, "traffic": None,
                      "ops_per_pair": ops, "pairs_evaluated": work_pairs,
