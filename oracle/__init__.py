@@ -17,6 +17,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import threading
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
@@ -42,32 +43,44 @@ def build(force: bool = False) -> str:
 
 
 _lib = None
+_lib_lock = threading.Lock()
 
 
 def lib() -> ctypes.CDLL:
+    """The loaded oracle library with its signatures declared.  Published only
+    once fully configured (the *_threaded helpers call it from many threads)."""
     global _lib
-    if _lib is None:
-        _lib = ctypes.CDLL(build())
-        P, I64, D, INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
-        _lib.oracle_inv_det_f64.argtypes = [P, I64, P, I64, P, I64]
-        _lib.oracle_inv_det_f32.argtypes = [P, I64, P, I64, P, I64]
-        _lib.oracle_gauss_jordan.argtypes = [P, P, P]
-        _lib.oracle_gauss_jordan.restype = INT
-        _lib.oracle_pair_distance.argtypes = [P, P, D]
-        _lib.oracle_pair_distance.restype = D
-        _lib.oracle_window_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
-        _lib.oracle_window_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
-        _lib.oracle_inv_det_blocks_f64.argtypes = [P, I64, INT, P, I64, I64]
-        _lib.oracle_inv_det_blocks_f32.argtypes = [P, I64, INT, P, I64, I64]
-        _lib.oracle_nlm_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
-        _lib.oracle_nlm_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
-        _lib.oracle_window_kl_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
-        _lib.oracle_window_kl_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
-        _lib.oracle_kl_distance.argtypes = [P, P, D]
-        _lib.oracle_kl_distance.restype = D
-        _lib.oracle_ldbl_mant_dig.restype = INT
-        _lib.oracle_quad_mant_dig.restype = INT
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        _lib_new = ctypes.CDLL(build())
+        _configure(_lib_new)
+        _lib = _lib_new
     return _lib
+
+
+def _configure(_lib: ctypes.CDLL) -> None:
+    P, I64, D, INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+    _lib.oracle_inv_det_f64.argtypes = [P, I64, P, I64, P, I64]
+    _lib.oracle_inv_det_f32.argtypes = [P, I64, P, I64, P, I64]
+    _lib.oracle_gauss_jordan.argtypes = [P, P, P]
+    _lib.oracle_gauss_jordan.restype = INT
+    _lib.oracle_pair_distance.argtypes = [P, P, D]
+    _lib.oracle_pair_distance.restype = D
+    _lib.oracle_window_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+    _lib.oracle_window_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+    _lib.oracle_inv_det_blocks_f64.argtypes = [P, I64, INT, P, I64, I64]
+    _lib.oracle_inv_det_blocks_f32.argtypes = [P, I64, INT, P, I64, I64]
+    _lib.oracle_nlm_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+    _lib.oracle_nlm_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+    _lib.oracle_window_kl_f64.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+    _lib.oracle_window_kl_f32.argtypes = [P, I64, I64, I64, INT, D, D, P, I64, P]
+    _lib.oracle_kl_distance.argtypes = [P, P, D]
+    _lib.oracle_kl_distance.restype = D
+    _lib.oracle_ldbl_mant_dig.restype = INT
+    _lib.oracle_quad_mant_dig.restype = INT
 
 
 def _ptr(a: np.ndarray) -> int:

@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 from . import _build
 
@@ -35,6 +36,7 @@ SIGNATURES = {
 }
 
 _lib = None
+_lib_lock = threading.Lock()
 
 
 class PolsarError(RuntimeError):
@@ -42,9 +44,15 @@ class PolsarError(RuntimeError):
 
 
 def lib() -> ctypes.CDLL:
-    """Load (building in-tree first if the .so is missing or stale)."""
+    """Load (building in-tree first if the .so is missing or stale).  The
+    handle is published only once every signature is declared, so threads
+    calling in concurrently never see an unconfigured library."""
     global _lib
-    if _lib is None:
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
         path = _build.TARGETS["libpolsar"]["out"]
         override = os.environ.get("POLSAR_LIB_OVERRIDE")  # development A/B builds only
         if override:
@@ -56,13 +64,14 @@ def lib() -> ctypes.CDLL:
             if not os.path.exists(path):
                 raise PolsarError(f"libpolsar.so is not built and cannot be built: {e}") from e
         try:
-            _lib = ctypes.CDLL(path)
+            handle = ctypes.CDLL(path)
         except OSError as e:
             raise PolsarError(f"cannot load {path}: {e}") from e
         for name, (res, args) in SIGNATURES.items():
-            fn = getattr(_lib, name)
+            fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
+        _lib = handle
     return _lib
 
 

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(K3_TX * K3_TY / K3_RB, 1)
 k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
              int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
              int alpha_is_2, S* __restrict__ out) {
-    extern __shared__ unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int HW = K3_TX + 2 * R;        // halo tile width
     const int HH = K3_TY + 2 * R;        // halo tile height
     const int HP = HW * HH;              // pixels in the halo tile
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(K3_TX * TY / RB, 1)
 k_nlm_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
           int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
           int alpha_is_2, S* __restrict__ out_w, S* __restrict__ out_z, int64_t ld_out) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int HW = K3_TX + 2 * R;
     const int HH = TY + 2 * R;
     const int HP = HW * HH;
@@ -631,7 +631,7 @@ template <typename S, typename WT, bool A2, int KIND = DIST_LOGDET>
 __global__ void __launch_bounds__(V3_THREADS, 1)
 k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows, int64_t row_begin,
                 int64_t row_end, int R, double alpha_d, S* __restrict__ out) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int XOFF = V3_XOFF, SW = V3_SW, CHP = V3_CHP;
     double* buf = reinterpret_cast<double*>(smem_raw);  // [2][V3_NP][V3_CH][SW]
     const int64_t P = slab_rows * width;                // workspace plane stride
@@ -961,27 +961,49 @@ struct KLPair {
     }
 };
 
+// Backward sums in shared memory (ACC forms of pass 1, window and KL): each
+// pair weight w(i, j) is added to j's backward sum as the fixed-point integer
+// round(w 2^44), split over two 32-bit counters (bits 22 and up, bits 0-21)
+// so the native shared-memory ATOMS.ADD serves: integer addition is exact
+// and associative, so the sums are bit-reproducible in any order and any
+// tiling.  Per target and tile at most 2R(R+1) <= 312 weights <= 1 (+ rounding)
+// arrive: the high counter stays below 2^31, the low one below 2^31.  Weights
+// of invalid (non-positive-definite) inputs are clamped to 256 first.
+constexpr float kFix = 17592186044416.0f;  // 2^44
+__device__ __forceinline__ long long fixed_w(float w) { return __float2ll_rn(fminf(w, 256.0f) * kFix); }
+__device__ __forceinline__ long long fixed_w(double w) { return __double2ll_rn(fmin(w, 256.0) * (double)kFix); }
+__device__ __forceinline__ void acc_add(unsigned* ah, int hp, int q, long long v) {
+    atomicAdd(ah + q, (unsigned)((unsigned long long)v >> 22));
+    atomicAdd(ah + hp + q, (unsigned)(v & 0x3fffff));
+}
+
 // Pass 1, one full window row (all 2R+1 neighbours valid for every owned
 // row): weights into row[] and, for owned in-image pairs, into the planes
-// wp[r] (advanced by one plane per neighbour).
-template <typename Pair, int RB, bool FULL>
+// wp[r] (advanced by one plane per neighbour), or (ACC) into the neighbours'
+// backward sums ah[qj + wx + R].
+template <typename Pair, int RB, bool FULL, bool ACC>
 __device__ __forceinline__ void fwd_full_row(const Pair& pr, const typename Pair::Rec (&ri)[RB],
                                              const typename Pair::T* rec, int R, int64_t gx,
                                              int64_t width, bool interior_x, const bool (&own)[RB],
                                              typename Pair::WT* (&wp)[RB], int64_t N,
-                                             typename Pair::WT (&row)[RB]) {
+                                             typename Pair::WT (&row)[RB], unsigned* ah, int hp, int qj) {
     // FULL: the CTA's whole tile is inside the image and the output rows, so
     // every pair is in-image and owned: no masks, unconditional stores
     using WT = typename Pair::WT;
 #pragma unroll kSymUnroll
-    for (int wx = -R; wx <= R; ++wx, rec += Pair::RS) {
+    for (int wx = -R; wx <= R; ++wx, rec += Pair::RS, ++qj) {
         typename Pair::Rec rj;
         Pair::load(rec, rj);
         const bool colok = FULL || interior_x || (gx + wx >= 0 && gx + wx < width);
+        long long v = 0;
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
             WT w = pr.weight(ri[r], rj);
-            if constexpr (FULL) {
+            if constexpr (ACC) {
+                if (!FULL) w = colok ? w : WT(0);
+                row[r] += w;
+                if (FULL || own[r]) v += fixed_w(w);
+            } else if constexpr (FULL) {
                 row[r] += w;
                 *wp[r] = w;
             } else {
@@ -989,8 +1011,9 @@ __device__ __forceinline__ void fwd_full_row(const Pair& pr, const typename Pair
                 row[r] += w;
                 if (colok && own[r]) *wp[r] = w;
             }
-            wp[r] += N;
+            if constexpr (!ACC) wp[r] += N;
         }
+        if constexpr (ACC) acc_add(ah, hp, qj, v);
     }
 }
 
@@ -998,11 +1021,11 @@ __device__ __forceinline__ void fwd_full_row(const Pair& pr, const typename Pair
 // neighbour wx and the weight, sum and store (post) of wx - 1 form one basic
 // block, so the scheduler overlaps them.  The first post is a no-op
 // (ok = false) and the sums keep wx order, so results equal fwd_full_row's.
-template <typename Pair, int RB>
+template <typename Pair, int RB, bool ACC>
 __device__ __forceinline__ void fwd_full_row_pipelined(
     const Pair& pr, const typename Pair::Rec (&ri)[RB], const typename Pair::T* rec, int R,
     int64_t gx, int64_t width, bool interior_x, const bool (&own)[RB], typename Pair::WT* (&wp)[RB],
-    int64_t N, typename Pair::WT (&row)[RB]) {
+    int64_t N, typename Pair::WT (&row)[RB], unsigned* ah, int hp, int qj) {
     using WT = typename Pair::WT;
     typename Pair::Q qp[RB];
 #pragma unroll
@@ -1020,37 +1043,56 @@ __device__ __forceinline__ void fwd_full_row_pipelined(
         typename Pair::Q q[RB];
 #pragma unroll
         for (int r = 0; r < RB; ++r) q[r] = pr.pre(ri[r], rj);
+        long long v = 0;
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
             WT w = pr.post(qp[r], ri[r], ap);
             w = okp ? w : WT(0);
             row[r] += w;
-            if (okp && own[r]) *wp[r] = w;
-            wp[r] += N;
+            if constexpr (ACC) {
+                if (own[r]) v += fixed_w(w);
+            } else {
+                if (okp && own[r]) *wp[r] = w;
+                wp[r] += N;
+            }
             qp[r] = q[r];
+        }
+        if constexpr (ACC) {
+            if (wx > -R) acc_add(ah, hp, qj + wx + R - 1, v);  // neighbour wx - 1
         }
         ap = Pair::aux(rj);
         okp = colok;
     }
+    long long v = 0;
 #pragma unroll
     for (int r = 0; r < RB; ++r) {  // the last neighbour's post
         WT w = pr.post(qp[r], ri[r], ap);
         w = okp ? w : WT(0);
         row[r] += w;
-        if (okp && own[r]) *wp[r] = w;
+        if constexpr (ACC) {
+            if (own[r]) v += fixed_w(w);
+        } else {
+            if (okp && own[r]) *wp[r] = w;
+        }
     }
+    if constexpr (ACC) acc_add(ah, hp, qj + 2 * R, v);
 }
 
-// Pass 1, generic over the pair policy.
-template <typename Pair, int TY, int RB>
+// Pass 1, generic over the pair policy.  ACC: instead of storing the pair
+// weights, accumulate every in-tile-halo neighbour's backward sum in shared
+// memory (fixed point, acc_add) and write the tile's halo-region sums to
+// part[tile][HP] (int64) at the end; pass 2 (k_window_bwd_acc) adds the <= 4
+// tiles' sums of each pixel.
+template <typename Pair, int TY, int RB, bool ACC = false>
 __global__ void __launch_bounds__(K3_TX * TY / RB, 1)
 k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64_t row_end, int R,
-             int64_t wpitch, typename Pair::WT* __restrict__ wbuf, double* __restrict__ fbuf) {
+             int64_t wpitch, typename Pair::WT* __restrict__ wbuf, double* __restrict__ fbuf,
+             long long* __restrict__ part) {
     using T = typename Pair::T;
     using WT = typename Pair::WT;
     using Rec = typename Pair::Rec;
     constexpr int RS = Pair::RS;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int HW = K3_TX + 2 * R;   // halo columns x0-R .. x0+TX-1+R
     const int HH = TY + R;          // halo rows y0 .. y0+TY-1+R (forward only)
     const int HP = HW * HH;
@@ -1059,11 +1101,17 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
 
     const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
     const int64_t y0 = row_begin + (int64_t)blockIdx.y * TY;
+    // ACC: the backward-sum counters follow the records (high words, then low)
+    unsigned* ah = reinterpret_cast<unsigned*>(sz + (size_t)RS * HP);
     for (int q = threadIdx.x; q < HP; q += blockDim.x) {
         int hy = q / HW, hx = q % HW;
         int64_t gy = y0 + hy, gx = x0 - R + hx;
         bool in = gy < slab_rows && gx >= 0 && gx < width;
         pr.fill(sz + RS * q, in ? gy * width + gx : 0, in);
+        if constexpr (ACC) {
+            ah[q] = 0u;
+            ah[HP + q] = 0u;
+        }
     }
     __syncthreads();
 
@@ -1100,18 +1148,23 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
 #pragma unroll
             for (int r = 0; r < RB; ++r) wp[r] = wbuf + (int64_t)fwd_index(wy - r, -R, R) * N + pi[r];
             POLSAR_CHECK(hy >= 0 && hy < HH && tx + 2 * R < HW);  // records wx = -R..R
+            const int qj = hy * HW + tx;  // backward-sum slot of neighbour wx = -R
             if constexpr (Pair::kPipeline)
-                fwd_full_row_pipelined<Pair, RB>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row);
+                fwd_full_row_pipelined<Pair, RB, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row,
+                                                      ah, HP, qj);
             else if (full)
-                fwd_full_row<Pair, RB, true>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row);
+                fwd_full_row<Pair, RB, true, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row,
+                                                  ah, HP, qj);
             else
-                fwd_full_row<Pair, RB, false>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row);
+                fwd_full_row<Pair, RB, false, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row,
+                                                   ah, HP, qj);
         } else {
             for (int wx = -R; wx <= R; ++wx, rec += RS) {
                 POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
                 Rec rj;
                 Pair::load(rec, rj);
                 const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+                long long v = 0;
 #pragma unroll
                 for (int r = 0; r < RB; ++r) {
                     const int dy = wy - r;
@@ -1119,9 +1172,14 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
                         WT w = pr.weight(ri[r], rj);
                         w = colok ? w : WT(0);
                         row[r] += w;
-                        if (colok && own[r]) wbuf[(int64_t)fwd_index(dy, wx, R) * N + pi[r]] = w;
+                        if constexpr (ACC) {
+                            if (own[r]) v += fixed_w(w);
+                        } else {
+                            if (colok && own[r]) wbuf[(int64_t)fwd_index(dy, wx, R) * N + pi[r]] = w;
+                        }
                     }
                 }
+                if constexpr (ACC) acc_add(ah, HP, hy * HW + tx + wx + R, v);
             }
         }
 #pragma unroll
@@ -1130,6 +1188,44 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
 #pragma unroll
     for (int r = 0; r < RB; ++r)
         if (gx < width && y0 + ty0 + r < row_end) fbuf[(y0 + ty0 + r) * width + gx] = acc[r];
+    if constexpr (ACC) {
+        __syncthreads();
+        long long* dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * HP;
+        for (int q = threadIdx.x; q < HP; q += blockDim.x)
+            dst[q] = (long long)(((unsigned long long)ah[q] << 22) + ah[HP + q]);
+    }
+}
+
+// Pass 2 of the ACC forms: W_j = 1 + F_j + 2^-44 (sum of the backward sums of
+// the <= 4 pass-1 tiles whose halo region holds j; integer, exact).  Tile
+// (bx, by) covers rows p0 + by TY .. + TY + R - 1 and columns 32 bx - R ..
+// 32 bx + 31 + R of its halo region.
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_window_bwd_acc(const long long* __restrict__ part, const double* __restrict__ fbuf, int64_t width,
+                 int64_t row_begin, int64_t row_end, int64_t p0, int R, int TY, int nbx, int nby,
+                 S* __restrict__ out) {
+    const int HW = K3_TX + 2 * R;
+    const int HP = HW * (TY + R);
+    const int64_t m = (row_end - row_begin) * width;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = row_begin + q / width, x = q % width;
+        const int64_t yr = y - p0;  // >= 0
+        // by: p0 + by TY <= y < p0 + by TY + TY + R ; bx: 32 bx - R <= x < 32 bx + 32 + R
+        const int64_t by_hi = yr / TY;
+        const int64_t by_lo = yr - TY - R + 1 > 0 ? (yr - TY - R + 1 + TY - 1) / TY : 0;
+        const int64_t bx_hi = (x + R) / K3_TX < nbx - 1 ? (x + R) / K3_TX : nbx - 1;
+        const int64_t bx_lo = x - K3_TX - R + 1 > 0 ? (x - K3_TX - R + 1 + K3_TX - 1) / K3_TX : 0;
+        long long sum = 0;
+        for (int64_t by = by_lo; by <= by_hi && by < nby; ++by)
+            for (int64_t bx = bx_lo; bx <= bx_hi; ++bx) {
+                const int64_t hy = yr - by * TY, hx = x - K3_TX * bx + R;
+                POLSAR_CHECK(hy >= 0 && hy < TY + R && hx >= 0 && hx < HW);
+                sum += part[(by * nbx + bx) * HP + hy * HW + hx];
+            }
+        out[q] = (S)__dadd_rn(__dadd_rn(1.0, fbuf[y * width + x]), (double)sum * (1.0 / (double)kFix));
+    }
 }
 
 // Pass 2: W_j = 1 + F_j + sum over backward neighbours, one thread per pixel.
@@ -1179,19 +1275,69 @@ size_t window_fwd_smem(int TY, int R) {
 
 // Launch pass 1 over rows [p0, re) (p0 = max(0, rb - R): the R rows above the
 // output rows hold the forward pairs that are their backward pairs).
-template <typename Pair, int TY, int RB>
+// Pass-1 tile grid over rows [p0, re): (nbx, nby) and the halo-region size
+// HP of a tile (also the ACC forms' backward-sum slots per tile).
+struct FwdGrid {
+    int64_t p0;
+    int nbx, nby, HP;
+};
+inline FwdGrid fwd_grid(int64_t width, int64_t rb, int64_t re, int R, int TY) {
+    FwdGrid g;
+    g.p0 = rb - R > 0 ? rb - R : 0;
+    g.nbx = (int)((width + K3_TX - 1) / K3_TX);
+    g.nby = (int)((re - g.p0 + TY - 1) / TY);
+    g.HP = (K3_TX + 2 * R) * (TY + R);
+    return g;
+}
+
+template <typename Pair, int TY, int RB, bool ACC = false>
 int launch_fwd(const Pair& pr, int64_t width, int64_t slab_rows, int64_t rb, int64_t re, int R,
-               typename Pair::WT* wbuf, double* fbuf, cudaStream_t s, const char* who) {
-    const int64_t p0 = rb - R > 0 ? rb - R : 0;
-    const size_t smem = window_fwd_smem<Pair>(TY, R);
-    auto kern = k_window_fwd<Pair, TY, RB>;
+               typename Pair::WT* wbuf, double* fbuf, cudaStream_t s, const char* who,
+               long long* part = nullptr) {
+    const FwdGrid fg = fwd_grid(width, rb, re, R, TY);
+    const size_t smem = window_fwd_smem<Pair>(TY, R) + (ACC ? 2 * sizeof(unsigned) * (size_t)fg.HP : 0);
+    auto kern = k_window_fwd<Pair, TY, RB, ACC>;
     if (smem > K3_SMEM_MAX ||
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return fail(POLSAR_ENOTSUP, who);
-    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - p0 + TY - 1) / TY));
-    kern<<<grid, K3_TX * TY / RB, smem, s>>>(pr, width, slab_rows, p0, re, R, weight_pitch<typename Pair::WT>(width),
-                                             wbuf, fbuf);
+    dim3 grid((unsigned)fg.nbx, (unsigned)fg.nby);
+    kern<<<grid, K3_TX * TY / RB, smem, s>>>(pr, width, slab_rows, fg.p0, re, R, weight_pitch<typename Pair::WT>(width),
+                                             wbuf, fbuf, part);
     return POLSAR_OK;
+}
+
+// shared memory of pass 1 in the ACC form (records + two counters per slot)
+template <typename Pair>
+size_t acc_fwd_smem(int TY, int R) {
+    return window_fwd_smem<Pair>(TY, R) + 2 * sizeof(unsigned) * (size_t)(K3_TX + 2 * R) * (TY + R);
+}
+
+template <typename S>
+void launch_bwd_acc(const long long* part, const double* fbuf, int64_t width, int64_t rb, int64_t re,
+                    int R, int TY, void* outv, cudaStream_t s) {
+    const FwdGrid fg = fwd_grid(width, rb, re, R, TY);
+    k_window_bwd_acc<S><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(part, fbuf, width, rb, re, fg.p0, R,
+                                                                        TY, fg.nbx, fg.nby, (S*)outv);
+}
+
+// workspace of the ACC forms: the prepass planes (pre_bytes) | F | the tiles'
+// backward sums (int64, HP per tile, over the whole slab's row range)
+inline size_t acc_sym_bytes(size_t pre_bytes, int64_t slab_rows, int64_t width, int R, int TY) {
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    const FwdGrid fg = fwd_grid(width, 0, slab_rows, R, TY);
+    return up(pre_bytes) + up((size_t)slab_rows * width * sizeof(double)) +
+           up((size_t)fg.nbx * fg.nby * fg.HP * sizeof(long long));
+}
+
+// Window / KL symmetric form: backward sums in shared memory (ACC, default)
+// or through the weight planes (POLSAR_WINDOW_PLANES=1, the A/B alternative).
+bool window_planes() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("POLSAR_WINDOW_PLANES");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
 }
 
 template <typename S, typename WT>
@@ -1228,13 +1374,27 @@ int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_ro
     WT* wbuf = (WT*)(ws + up(n * sizeof(WT)) + up(n * sizeof(double)));
     k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
     const double alpha = looks / (2.0 * h);
+    const char* who = "polsar_window_distance: shared memory request too large";
+    if (!window_planes() && acc_fwd_smem<LogDetPair<S, T, WT, 1>>(POLSAR_SYM_TY, R) <= K3_SMEM_MAX) {
+        long long* part = (long long*)wbuf;  // (same offset: g | F | tile sums)
+        int rc = alpha == 2.0
+                     ? launch_fwd<LogDetPair<S, T, WT, 1>, POLSAR_SYM_TY, POLSAR_SYM_RB, true>(
+                           LogDetPair<S, T, WT, 1>{z, ld, g, (WT)alpha, true}, width, slab_rows, rb, re, R,
+                           nullptr, fbuf, s, who, part)
+                     : launch_fwd<LogDetPair<S, T, WT, 0>, POLSAR_SYM_TY, POLSAR_SYM_RB, true>(
+                           LogDetPair<S, T, WT, 0>{z, ld, g, (WT)alpha, false}, width, slab_rows, rb, re, R,
+                           nullptr, fbuf, s, who, part);
+        if (rc != POLSAR_OK) return rc;
+        launch_bwd_acc<S>(part, fbuf, width, rb, re, R, POLSAR_SYM_TY, outv, s);
+        return launch_check("polsar_window_distance: launch failed");
+    }
     int rc = alpha == 2.0
                  ? launch_fwd<LogDetPair<S, T, WT, 1>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
                        LogDetPair<S, T, WT, 1>{z, ld, g, (WT)alpha, true}, width, slab_rows, rb, re, R,
-                       wbuf, fbuf, s, "polsar_window_distance: shared memory request too large")
+                       wbuf, fbuf, s, who)
                  : launch_fwd<LogDetPair<S, T, WT, 0>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
                        LogDetPair<S, T, WT, 0>{z, ld, g, (WT)alpha, false}, width, slab_rows, rb, re, R,
-                       wbuf, fbuf, s, "polsar_window_distance: shared memory request too large");
+                       wbuf, fbuf, s, who);
     if (rc != POLSAR_OK) return rc;
     launch_bwd<S, WT>(wbuf, fbuf, width, slab_rows, rb, re, R, outv, s);
     return launch_check("polsar_window_distance: launch failed");
@@ -1261,6 +1421,15 @@ int launch_window_kl_sym(const void* zv, int64_t ld, int64_t width, int64_t slab
     WT* wbuf = (WT*)(ws + up((size_t)n * V3_NP * sizeof(double)) + up(n * sizeof(double)));
     k_window_prep_kl<S><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, prep);
     KLPair<WT> pr{prep, n, (WT)(looks / h)};
+    // (KL at R = 12: records + counters exceed shared memory; the plane form serves)
+    if (!window_planes() && acc_fwd_smem<KLPair<WT>>(16, R) <= K3_SMEM_MAX) {
+        long long* part = (long long*)wbuf;
+        int rc = launch_fwd<KLPair<WT>, 16, 2, true>(pr, width, slab_rows, rb, re, R, nullptr, fbuf, s,
+                                                      "polsar_window_kl: shared memory request too large", part);
+        if (rc != POLSAR_OK) return rc;
+        launch_bwd_acc<S>(part, fbuf, width, rb, re, R, 16, outv, s);
+        return launch_check("polsar_window_kl: launch failed");
+    }
     int rc = launch_fwd<KLPair<WT>, 16, 2>(pr, width, slab_rows, rb, re, R, wbuf, fbuf, s,
                                             "polsar_window_kl: shared memory request too large");
     if (rc != POLSAR_OK) return rc;
@@ -1698,6 +1867,9 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radiu
     if (radius <= V3_RMAX) {
         b = std::max(b, wt64 ? window_sym_bytes<double>(slab_rows, width, radius)
                              : window_sym_bytes<float>(slab_rows, width, radius));
+        b = std::max(b, acc_sym_bytes((size_t)n * (wt64 ? 8 : 4), slab_rows, width, radius, POLSAR_SYM_TY));
+        if (dtype != POLSAR_F32_PLAIN)
+            b = std::max(b, acc_sym_bytes((size_t)n * V3_NP * sizeof(double), slab_rows, width, radius, 16));
         if (dtype != POLSAR_F32_PLAIN)
             b = std::max(b, wt64 ? kl_sym_bytes<double>(slab_rows, width, radius)
                                  : kl_sym_bytes<float>(slab_rows, width, radius));

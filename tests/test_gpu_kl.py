@@ -19,7 +19,8 @@ TOL = {torch.float32: 2e-5, torch.float64: 2e-9}
 
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
-@pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 290), 3), ((20, 70), 0)])
+@pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 290), 3), ((20, 70), 0), ((50, 60), 12),
+                                          ((45, 7), 1), ((1, 90), 5)])
 def test_window_kl_parity(cuda, dt, shape, radius):
     h, w = shape
     z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda).to(dt)

@@ -27,7 +27,8 @@ def clipped_counts(h, w, r):
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
 @pytest.mark.parametrize("shape,radius", [((96, 80), 11), ((37, 53), 3), ((20, 70), 0), ((150, 33), 11),
-                                          ((300, 270), 11), ((40, 45), 14)])
+                                          ((300, 270), 11), ((40, 45), 14), ((60, 100), 12), ((45, 7), 1),
+                                          ((1, 90), 5)])
 def test_window_parity(cuda, dt, shape, radius):
     h, w = shape
     cfg = configs.get("c5").scaled(h, w)
@@ -93,12 +94,14 @@ def test_window_c5_sampled(cuda):
     assert np.all(np.isfinite(got)) and got.min() >= 1 - 1e-6 and got.max() <= 529 + 1e-3
 
 
-@pytest.mark.parametrize("variant", ["2", "3"])
+@pytest.mark.parametrize("variant", ["2", "3", "planes"])
 def test_window_variant_subprocess(cuda, variant):
     """The alternative kernels (POLSAR_WINDOW_VARIANT=2: the direct form over
-    ordered pairs; 3: the expansion form; read once per process) against the
-    oracle in a child process: the log-det window sum, and the KL window sum
-    (both variants run KL on the streaming expansion kernel)."""
+    ordered pairs; 3: the expansion form; POLSAR_WINDOW_PLANES=1: the
+    symmetric form through the weight planes instead of the shared-memory
+    backward sums; read once per process) against the oracle in a child
+    process: the log-det window sum, and the KL window sum (variants 2 and 3
+    run KL on the streaming expansion kernel)."""
     import os
     import subprocess
     import sys
@@ -120,7 +123,8 @@ for dt, tol, tol_kl in ((torch.float32, 2e-5, 2e-5), (torch.float64, 4e-10, 2e-9
     assert e <= tol_kl, ("kl", dt, e)
 print("ok")
 '''
-    env = dict(os.environ, POLSAR_WINDOW_VARIANT=variant)
+    env = dict(os.environ, **({"POLSAR_WINDOW_PLANES": "1"} if variant == "planes"
+                              else {"POLSAR_WINDOW_VARIANT": variant}))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=300)
