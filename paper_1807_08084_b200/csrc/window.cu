@@ -961,6 +961,65 @@ struct KLPair {
     }
 };
 
+// KL with fp32 storage: Z is exact in fp32, so the record keeps X (9 fp64)
+// and Z (9 fp32, widened on load): 112 bytes instead of 144 (KL's pass 1 is
+// bound by shared-memory bandwidth).  Same arithmetic as KLPair.
+template <typename WT_>
+struct KLPairF {
+    using T = double;
+    using WT = WT_;
+    static constexpr int RS = 14;  // 112 bytes: X0..X8 (fp64), Z0..Z8 (fp32) at byte 72, pad
+    using Rec = typename KLPair<WT_>::Rec;
+    const double* ws;  // prep planes 0..8 = Z, 9..17 = X, plane stride P
+    int64_t P;
+    WT lk;             // L / h
+    __device__ __forceinline__ void fill(double* rec, int64_t p, bool in) const {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) rec[k] = in ? ws[(9 + k) * P + p] : 0.0;
+        float* zf = reinterpret_cast<float*>(rec + 9);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) zf[k] = in ? (float)ws[k * P + p] : 0.0f;  // exact: Z came from fp32
+        zf[9] = 0.0f;
+    }
+    __device__ __forceinline__ static void load(const double* rec, Rec& r) {
+        const double2* v = reinterpret_cast<const double2*>(rec);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 u = v[k];
+            r.x[2 * k] = u.x;
+            r.x[2 * k + 1] = u.y;
+        }
+        r.x[8] = rec[8];
+        const float2 a = *reinterpret_cast<const float2*>(rec + 9);          // byte 72
+        const float4 b = *reinterpret_cast<const float4*>(rec + 10);         // byte 80
+        const float4 c = *reinterpret_cast<const float4*>(rec + 12);         // byte 96
+        r.z[0] = a.x; r.z[1] = a.y; r.z[2] = b.x; r.z[3] = b.y;
+        r.z[4] = b.z; r.z[5] = b.w; r.z[6] = c.x; r.z[7] = c.y; r.z[8] = c.z;
+    }
+    static constexpr bool kPipeline = true;
+    using Q = double;
+    using Aux = int;
+    __device__ __forceinline__ Q pre(const Rec& i, const Rec& j) const {
+        double A = __dmul_rn(i.x[0], j.z[0]);
+        double B = __dmul_rn(i.z[0], j.x[0]);
+#pragma unroll
+        for (int k = 1; k < 9; ++k) {
+            A = __fma_rn(i.x[k], j.z[k], A);
+            B = __fma_rn(i.z[k], j.x[k], B);
+        }
+        return __dadd_rn(A, B);
+    }
+    __device__ __forceinline__ static Aux aux(const Rec&) { return 0; }
+    __device__ __forceinline__ WT post(Q T, const Rec&, Aux) const { return weight_kl<WT>(T, lk); }
+    __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
+        return post(pre(i, j), i, aux(j));
+    }
+};
+
+#ifndef POLSAR_KLF_TY
+#define POLSAR_KLF_TY 24
+#endif
+
 // Backward sums in shared memory (ACC forms of pass 1, window and KL): each
 // pair weight w(i, j) is added to j's backward sum as the fixed-point integer
 // round(w 2^44), split over two 32-bit counters (bits 22 and up, bits 0-21)
@@ -1421,6 +1480,19 @@ int launch_window_kl_sym(const void* zv, int64_t ld, int64_t width, int64_t slab
     WT* wbuf = (WT*)(ws + up((size_t)n * V3_NP * sizeof(double)) + up(n * sizeof(double)));
     k_window_prep_kl<S><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, prep);
     KLPair<WT> pr{prep, n, (WT)(looks / h)};
+    if constexpr (sizeof(S) == 4) {  // fp32 storage: the 112-byte records
+        constexpr int TYF = POLSAR_KLF_TY;
+        KLPairF<WT> pf{prep, n, (WT)(looks / h)};
+        if (!window_planes() && acc_fwd_smem<KLPairF<WT>>(TYF, R) <= K3_SMEM_MAX) {
+            long long* part = (long long*)wbuf;
+            int rc = launch_fwd<KLPairF<WT>, TYF, 2, true>(pf, width, slab_rows, rb, re, R, nullptr, fbuf, s,
+                                                            "polsar_window_kl: shared memory request too large",
+                                                            part);
+            if (rc != POLSAR_OK) return rc;
+            launch_bwd_acc<S>(part, fbuf, width, rb, re, R, TYF, outv, s);
+            return launch_check("polsar_window_kl: launch failed");
+        }
+    }
     // (KL at R = 12: records + counters exceed shared memory; the plane form serves)
     if (!window_planes() && acc_fwd_smem<KLPair<WT>>(16, R) <= K3_SMEM_MAX) {
         long long* part = (long long*)wbuf;
@@ -1868,8 +1940,11 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radiu
         b = std::max(b, wt64 ? window_sym_bytes<double>(slab_rows, width, radius)
                              : window_sym_bytes<float>(slab_rows, width, radius));
         b = std::max(b, acc_sym_bytes((size_t)n * (wt64 ? 8 : 4), slab_rows, width, radius, POLSAR_SYM_TY));
-        if (dtype != POLSAR_F32_PLAIN)
+        if (dtype != POLSAR_F32_PLAIN) {
             b = std::max(b, acc_sym_bytes((size_t)n * V3_NP * sizeof(double), slab_rows, width, radius, 16));
+            b = std::max(b, acc_sym_bytes((size_t)n * V3_NP * sizeof(double), slab_rows, width, radius,
+                                          POLSAR_KLF_TY));
+        }
         if (dtype != POLSAR_F32_PLAIN)
             b = std::max(b, wt64 ? kl_sym_bytes<double>(slab_rows, width, radius)
                                  : kl_sym_bytes<float>(slab_rows, width, radius));
