@@ -55,7 +55,11 @@ k_window_prep(const S* __restrict__ z, int64_t ld, int64_t n, WT* __restrict__ g
 #pragma unroll
         for (int k = 0; k < 9; ++k) v[k] = (T)z[k * ld + p];
         T dz = det_eq6<T>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8]);
-        g[p] = (WT)(T(1) / MUL(T(8), dz));
+        // NaN marks a pixel that is not positive definite (or not finite): every
+        // weight it enters becomes NaN, and so does W of every pixel whose
+        // window holds it
+        const WT gv = (WT)(T(1) / MUL(T(8), dz));
+        g[p] = (dz > T(0) && gv < WT(INFINITY)) ? gv : WT(NAN);
     }
 }
 
@@ -473,8 +477,10 @@ k_window_prep_kl(const S* __restrict__ z, int64_t ld, int64_t n, double* __restr
         ws[3 * P + p] = m.cr; ws[4 * P + p] = m.ci; ws[5 * P + p] = m.d;
         ws[6 * P + p] = m.er; ws[7 * P + p] = m.ei; ws[8 * P + p] = m.f;
         const double wk[9] = {1, 2, 2, 2, 2, 1, 2, 2, 1};
+        // X = NaN marks a pixel that is not positive definite (as g in k_window_prep)
+        const bool ok = det > 0.0 && t < INFINITY;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) ws[(9 + k) * P + p] = wk[k] * x[k];
+        for (int k = 0; k < 9; ++k) ws[(9 + k) * P + p] = ok ? wk[k] * x[k] : NAN;
         ws[18 * P + p] = 0.0;
         ws[19 * P + p] = 0.0;
     }
@@ -891,6 +897,8 @@ struct LogDetPair {
         rec[9] = pack_g<T, WT>(in ? g[p] : WT(0));
     }
     __device__ __forceinline__ static void load(const T* rec, Rec& r) { load_rec(rec, r.z, r.g); }
+    // (k_window_prep's NaN mark)
+    __device__ __forceinline__ static bool invalid(const Rec& r) { return !(r.g > WT(0)); }
     // weight = post(pre(i, j), i, aux(j)): pre is the FP64 part (det of
     // S = Z_i + Z_j by Eq. 6), post the fp32 weight (same arithmetic as pair_w)
     static constexpr bool kPipeline = false;  // measured: pipelining costs 4 % here
@@ -942,6 +950,7 @@ struct KLPair {
         }
     }
     static constexpr bool kPipeline = true;  // measured: 4.79 -> 4.43 ms on c5
+    __device__ __forceinline__ static bool invalid(const Rec& r) { return r.x[0] != r.x[0]; }  // NaN mark
     using Q = double;
     using Aux = int;
     __device__ __forceinline__ Q pre(const Rec& i, const Rec& j) const {
@@ -997,6 +1006,7 @@ struct KLPairF {
         r.z[4] = b.z; r.z[5] = b.w; r.z[6] = c.x; r.z[7] = c.y; r.z[8] = c.z;
     }
     static constexpr bool kPipeline = true;
+    __device__ __forceinline__ static bool invalid(const Rec& r) { return r.x[0] != r.x[0]; }  // NaN mark
     using Q = double;
     using Aux = int;
     __device__ __forceinline__ Q pre(const Rec& i, const Rec& j) const {
@@ -1025,12 +1035,18 @@ struct KLPairF {
 // round(w 2^44), split over two 32-bit counters (bits 22 and up, bits 0-21)
 // so the native shared-memory ATOMS.ADD serves: integer addition is exact
 // and associative, so the sums are bit-reproducible in any order and any
-// tiling.  Per target and tile at most 2R(R+1) <= 312 weights <= 1 (+ rounding)
-// arrive: the high counter stays below 2^31, the low one below 2^31.  Weights
-// of invalid (non-positive-definite) inputs are clamped to 256 first.
+// tiling.  Per target and tile at most 2R(R+1) <= 312 weights <= 1 arrive
+// (positive-definite inputs: d >= 0): the high counter stays below 2^31, and
+// the low one, fed < 2^22 per add, below 2^30.1.  Bit 31 of the low counter
+// is a NaN flag: a pixel marked invalid by the prepass (NaN g or X) sets it on
+// its own slot and on all its forward targets, so W comes out NaN exactly on
+// the pixels whose window holds it (its forward-pair weights are NaN too and
+// make F NaN; the integers they add to flagged slots are discarded).
 constexpr float kFix = 17592186044416.0f;  // 2^44
-__device__ __forceinline__ long long fixed_w(float w) { return __float2ll_rn(fminf(w, 256.0f) * kFix); }
-__device__ __forceinline__ long long fixed_w(double w) { return __double2ll_rn(fmin(w, 256.0) * (double)kFix); }
+constexpr unsigned kBadBit = 0x80000000u;
+constexpr long long kBadSum = (long long)(1ull << 63);  // a flagged tile sum in part[]
+__device__ __forceinline__ long long fixed_w(float w) { return __float2ll_rn(w * kFix); }
+__device__ __forceinline__ long long fixed_w(double w) { return __double2ll_rn(w * (double)kFix); }
 __device__ __forceinline__ void acc_add(unsigned* ah, int hp, int q, long long v) {
     atomicAdd(ah + q, (unsigned)((unsigned long long)v >> 22));
     atomicAdd(ah + hp + q, (unsigned)(v & 0x3fffff));
@@ -1191,6 +1207,18 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
     }
     const bool interior_x = (x0 - R >= 0) && (x0 + K3_TX + R <= width);
     const bool full = interior_x && y0 + TY <= row_end;  // CTA-uniform
+    if constexpr (ACC) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            if (own[r] && Pair::invalid(ri[r])) {  // rare: flag the pixel and its forward targets
+                const int q0 = (ty0 + r) * HW + (tx + R);
+                atomicOr(ah + HP + q0, kBadBit);
+                for (int dy = 0; dy <= R; ++dy)
+                    for (int dx = (dy == 0 ? 1 : -R); dx <= R; ++dx)
+                        atomicOr(ah + HP + q0 + dy * HW + dx, kBadBit);
+            }
+        }
+    }
 
     for (int wy = 0; wy <= R + RB - 1; ++wy) {
         const int64_t gyj = y0 + ty0 + wy;
@@ -1250,8 +1278,10 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
     if constexpr (ACC) {
         __syncthreads();
         long long* dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * HP;
-        for (int q = threadIdx.x; q < HP; q += blockDim.x)
-            dst[q] = (long long)(((unsigned long long)ah[q] << 22) + ah[HP + q]);
+        for (int q = threadIdx.x; q < HP; q += blockDim.x) {
+            const unsigned lo = ah[HP + q];
+            dst[q] = (lo & kBadBit) ? kBadSum : (long long)(((unsigned long long)ah[q] << 22) + lo);
+        }
     }
 }
 
@@ -1277,13 +1307,17 @@ k_window_bwd_acc(const long long* __restrict__ part, const double* __restrict__ 
         const int64_t bx_hi = (x + R) / K3_TX < nbx - 1 ? (x + R) / K3_TX : nbx - 1;
         const int64_t bx_lo = x - K3_TX - R + 1 > 0 ? (x - K3_TX - R + 1 + K3_TX - 1) / K3_TX : 0;
         long long sum = 0;
+        bool bad = false;
         for (int64_t by = by_lo; by <= by_hi && by < nby; ++by)
             for (int64_t bx = bx_lo; bx <= bx_hi; ++bx) {
                 const int64_t hy = yr - by * TY, hx = x - K3_TX * bx + R;
                 POLSAR_CHECK(hy >= 0 && hy < TY + R && hx >= 0 && hx < HW);
-                sum += part[(by * nbx + bx) * HP + hy * HW + hx];
+                const long long t = part[(by * nbx + bx) * HP + hy * HW + hx];
+                bad = bad || t == kBadSum;
+                sum += t;
             }
-        out[q] = (S)__dadd_rn(__dadd_rn(1.0, fbuf[y * width + x]), (double)sum * (1.0 / (double)kFix));
+        const double wb = bad ? __longlong_as_double(0x7ff8000000000000ll) : (double)sum * (1.0 / (double)kFix);
+        out[q] = (S)__dadd_rn(__dadd_rn(1.0, fbuf[y * width + x]), wb);
     }
 }
 

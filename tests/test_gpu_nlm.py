@@ -129,3 +129,18 @@ print("ok")
     res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=300)
     assert res.returncode == 0 and "ok" in res.stdout, res.stdout + res.stderr
+
+
+def test_nlm_nonfinite_input_propagates(cuda):
+    """A NaN pixel makes W and Zhat NaN exactly on the pixels whose window holds it."""
+    h, w, r = 40, 45, 5
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda).clone()
+    yb, xb = 20, 22
+    z[:, yb * w + xb] = float("nan")
+    zhat, W = P.nlm_filter(z, h, w, radius=r)
+    W = W.cpu().numpy().reshape(h, w)
+    zh = zhat.cpu().numpy().reshape(9, h, w)
+    ys, xs = np.mgrid[0:h, 0:w]
+    near = (np.abs(ys - yb) <= r) & (np.abs(xs - xb) <= r)
+    assert np.all(np.isnan(W[near])) and np.all(np.isfinite(W[~near]))
+    assert np.all(np.isnan(zh[:, near])) and np.all(np.isfinite(zh[:, ~near]))

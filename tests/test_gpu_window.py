@@ -129,3 +129,19 @@ print("ok")
     res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=300)
     assert res.returncode == 0 and "ok" in res.stdout, res.stdout + res.stderr
+
+
+@pytest.mark.parametrize("fn", ["window_distance", "window_kl"])
+def test_window_nonfinite_input_propagates(cuda, fn):
+    """A NaN pixel makes W NaN exactly on the pixels whose window holds it
+    (its forward pairs reach F, its backward pairs flag the shared-memory
+    sums), and nowhere else."""
+    h, w, r = 40, 45, 5
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda).clone()
+    yb, xb = 20, 22
+    z[:, yb * w + xb] = float("nan")
+    got = getattr(P, fn)(z, h, w, radius=r).cpu().numpy().reshape(h, w)
+    ys, xs = np.mgrid[0:h, 0:w]
+    near = (np.abs(ys - yb) <= r) & (np.abs(xs - xb) <= r)
+    assert np.all(np.isnan(got[near]))
+    assert np.all(np.isfinite(got[~near]))
