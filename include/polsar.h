@@ -107,9 +107,10 @@ int polsar_inv_det_blocks(const void* z, void* out, uint8_t* status, int64_t n, 
 
 /* polsar_window_workspace_bytes -- bytes of device workspace the window
  * entry points (polsar_window_distance, polsar_nlm_filter, polsar_window_kl)
- * need for a slab of slab_rows x width pixels at this radius and dtype.
- * (The default symmetric window kernel stores the 2R(R+1) forward pair
- * weights of every pixel: ~1.07 KB per pixel at R = 11, fp32 weights.) */
+ * need for a slab of slab_rows x width pixels at this radius and dtype: the
+ * largest need of the three.  (polsar_nlm_filter stores the 2R(R+1) forward
+ * pair weights of every pixel, ~1.07 KB per pixel at R = 11 with fp32
+ * weights; the default window and KL kernels need ~40 B per pixel.) */
 size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radius, int dtype);
 
 /* polsar_window_distance -- non-local-means search-window sum (the workload
@@ -128,7 +129,11 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radiu
  *   workspace : device, polsar_window_workspace_bytes(slab_rows, width, radius, dtype)
  *   dtype     : POLSAR_F32 (fp32 storage, fp64 pair determinant, fp32
  *               weight) or POLSAR_F64 (fp64 throughout), or the _PLAIN
- *               variants (storage precision throughout). */
+ *               variants (storage precision throughout).
+ * Pixels must be Hermitian positive definite: a pixel whose determinant is
+ * not positive or not finite makes W NaN on every pixel whose window holds it
+ * (likewise for polsar_window_kl and both outputs of polsar_nlm_filter).
+ * Results are bit-reproducible: any slab decomposition gives the same bits. */
 int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
                            int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
                            double h, void* workspace, void* out, int dtype, void* cuda_stream);
