@@ -865,7 +865,7 @@ __device__ __forceinline__ int fwd_index(int dy, int dx, int R) {
 #define POLSAR_SYM_RB 2
 #endif
 #ifndef POLSAR_SYM_UNROLL
-#define POLSAR_SYM_UNROLL 1
+#define POLSAR_SYM_UNROLL 2
 #endif
 constexpr int kSymUnroll = POLSAR_SYM_UNROLL;
 
@@ -901,7 +901,10 @@ struct LogDetPair {
     __device__ __forceinline__ static bool invalid(const Rec& r) { return !(r.g > WT(0)); }
     // weight = post(pre(i, j), i, aux(j)): pre is the FP64 part (det of
     // S = Z_i + Z_j by Eq. 6), post the fp32 weight (same arithmetic as pair_w)
-    static constexpr bool kPipeline = false;  // measured: pipelining costs 4 % here
+#ifndef POLSAR_LOGDET_PIPELINE
+#define POLSAR_LOGDET_PIPELINE 0
+#endif
+    static constexpr bool kPipeline = POLSAR_LOGDET_PIPELINE;  // measured: pipelining costs 4 % here
     using Q = T;
     using Aux = WT;
     __device__ __forceinline__ Q pre(const Rec& i, const Rec& j) const {
@@ -1833,9 +1836,14 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ C
 #pragma unroll
                     for (int k = 0; k < 9; ++k) pz[r][k] = ADD(pz[r][k], zr[k]);
                 }
-                tw[r] = __dadd_rn(tw[r], (double)pw[r]);
+                // a row that does not pair with this window row ran on zero weights
+                // but its Z (0 * NaN): skip it
+                const int64_t dyr = gy - (y0 + r);
+                if (y0 + r < row_end && dyr >= -R && dyr <= R) {
+                    tw[r] = __dadd_rn(tw[r], (double)pw[r]);
 #pragma unroll
-                for (int k = 0; k < 9; ++k) tz[r][k] = __dadd_rn(tz[r][k], (double)pz[r][k]);
+                    for (int k = 0; k < 9; ++k) tz[r][k] = __dadd_rn(tz[r][k], (double)pz[r][k]);
+                }
             }
         }
         __syncthreads();  // stage q % NS and ring slot q % NLM_NZ are refilled from row q + 1
