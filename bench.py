@@ -437,6 +437,23 @@ def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
                              (", error-free Alg. 2" if algo == "adjugate" else "")}
     del z4, o4, s4
     torch.cuda.empty_cache()
+    # K5: 3-band block-diagonal pixels of c3's law,
+    # 1e8 px (2500 of c3's rows per band), fp32 storage; (27 + 29) * 4 + 1 B / pixel
+    cb = configs.get("c3").scaled(2500)
+    nb = 3
+    with torch.cuda.stream(stream):
+        zb = wishart.generate_bands(cb, nb, device=dev)
+        ob = torch.empty((9 * nb + 2, cb.n), dtype=zb.dtype, device=dev)
+        sb = torch.empty(cb.n, dtype=torch.uint8, device=dev)
+    stream.synchronize()
+    t = _time_kernel(torch, stream, lambda: P.polsar_inv_det_blocks(zb, ob, nb, sb, stream=stream),
+                     max(3, steps // 2))
+    bpp = (9 * nb + 9 * nb + 2) * zb.element_size() + 1
+    gbs = cb.n * bpp / t / 1e9
+    res["blocks_c3_3bands"] = {"pixels_per_s": cb.n / t, "ms": t * 1e3, "GB/s": gbs, "frac_hbm": gbs / peak,
+                               "bytes_per_pixel": bpp, "mode": "3 bands x c3 law, 1e8 px, fp32 storage"}
+    del zb, ob, sb
+    torch.cuda.empty_cache()
     # K3: BASELINE configs[4] window sum on one GPU
     c5 = configs.get("c5")
     with torch.cuda.stream(stream):
@@ -454,6 +471,16 @@ def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
         res[f"window_c5{'_plain' if plain else ''}"] = {
             "pairs_per_s": pairs / t, "ms": t * 1e3, "pairs": pairs,
             "mode": "fp32 storage, fp32 weight, " + ("fp32 pair det" if plain else "fp64 pair det")}
+    # K6 (KL window) and K4 (NLM filter) on the same c5 input
+    t = _time_kernel(torch, stream, lambda: P.polsar_window_kl(
+        z5, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, w5, stream=stream), steps)
+    res["kl_window_c5"] = {"pairs_per_s": pairs / t, "ms": t * 1e3, "pairs": pairs,
+                           "mode": "symmetric Wishart KL, fp32 storage, fp64 trace products"}
+    zn = torch.empty((9, c5.n), dtype=z5.dtype, device=dev)
+    t = _time_kernel(torch, stream, lambda: P.polsar_nlm_filter(
+        z5, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, zn, w5, stream=stream), steps)
+    res["nlm_c5"] = {"pairs_per_s": pairs / t, "ms": t * 1e3, "pairs": pairs,
+                     "mode": "NLM output (W and Zhat), fp32 storage, fp64 pair det"}
     return res
 
 
