@@ -1602,8 +1602,12 @@ constexpr int NLM_ZW = NLM_TX + 2 * V3_RMAX;   // staged Z columns x0 - 12 .. x0
 // (12 floats / 10 doubles; strides of 12 and 20 words keep the 16-byte
 // loads of 8 consecutive lanes on distinct banks)
 template <typename S>
+#ifndef POLSAR_NLM_REC9
+#define POLSAR_NLM_REC9 1
+#endif
 struct NlmRec {
-    static constexpr int n = sizeof(S) == 4 ? 12 : 10;
+    // (POLSAR_NLM_REC9: fp32 records unpadded, 9 words, read as 9 scalars)
+    static constexpr int n = sizeof(S) == 4 ? (POLSAR_NLM_REC9 ? 9 : 12) : 10;
 };
 constexpr int NLM_OOB = -(1 << 30);            // a TMA coordinate whose tile is all zero-fill
 
@@ -1653,7 +1657,7 @@ __device__ __forceinline__ int64_t nlm_tile_coord(int64_t gy, int64_t yi, int wx
 template <typename WT>
 size_t nlm_smem_bytes(int R, int RB, int NS, size_t s_bytes) {
     return 128 + (size_t)NS * RB * (2 * R + 1) * NLM_TX * sizeof(WT) +
-           (size_t)NLM_NZ * NLM_ZW * (s_bytes == 4 ? 12 : 10) * s_bytes;
+           (size_t)NLM_NZ * NLM_ZW * (s_bytes == 4 ? NlmRec<float>::n : NlmRec<double>::n) * s_bytes;
 }
 
 // One window row for one thread: K = 0 all rows backward, 1 all forward,
@@ -1661,11 +1665,16 @@ size_t nlm_smem_bytes(int R, int RB, int NS, size_t s_bytes) {
 // dx < 0 and forward for dx > 0; its dx = 0 tile is zero); EDGE masks
 // out-of-image columns.
 __device__ __forceinline__ void nlm_load_rec(const float* p, float (&zj)[9]) {
+#if POLSAR_NLM_REC9
+#pragma unroll
+    for (int k = 0; k < 9; ++k) zj[k] = p[k];
+#else
     const float4 a = reinterpret_cast<const float4*>(p)[0];
     const float4 b = reinterpret_cast<const float4*>(p)[1];
     zj[0] = a.x; zj[1] = a.y; zj[2] = a.z; zj[3] = a.w;
     zj[4] = b.x; zj[5] = b.y; zj[6] = b.z; zj[7] = b.w;
     zj[8] = p[8];
+#endif
 }
 __device__ __forceinline__ void nlm_load_rec(const double* p, double (&zj)[9]) {
 #pragma unroll
