@@ -1032,6 +1032,9 @@ struct KLPairF {
 #ifndef POLSAR_KLF_TY
 #define POLSAR_KLF_TY 24
 #endif
+#ifndef POLSAR_KLF_RB
+#define POLSAR_KLF_RB 2
+#endif
 
 // Backward sums in shared memory (ACC forms of pass 1, window and KL): each
 // pair weight w(i, j) is added to j's backward sum as the fixed-point integer
@@ -1522,7 +1525,7 @@ int launch_window_kl_sym(const void* zv, int64_t ld, int64_t width, int64_t slab
         KLPairF<WT> pf{prep, n, (WT)(looks / h)};
         if (!window_planes() && acc_fwd_smem<KLPairF<WT>>(TYF, R) <= K3_SMEM_MAX) {
             long long* part = (long long*)wbuf;
-            int rc = launch_fwd<KLPairF<WT>, TYF, 2, true>(pf, width, slab_rows, rb, re, R, nullptr, fbuf, s,
+            int rc = launch_fwd<KLPairF<WT>, TYF, POLSAR_KLF_RB, true>(pf, width, slab_rows, rb, re, R, nullptr, fbuf, s,
                                                             "polsar_window_kl: shared memory request too large",
                                                             part);
             if (rc != POLSAR_OK) return rc;
