@@ -1644,17 +1644,18 @@ __device__ __forceinline__ void nlm_stage_row(S* dst, const S* __restrict__ z, i
 template <int AL>
 __host__ __device__ __forceinline__ int nlm_mis(int wx) { return wx & (AL - 1); }
 
-// TMA coordinate (element index in the flattened weight buffer, a multiple
-// of AL) of the tile of owned row yi at dx for window row gy.
+// TMA coordinates (pixel index within the plane, a multiple of AL; plane)
+// of the tile of owned row yi at dx for window row gy; plane NLM_OOB when
+// the row does not pair (the tile zero-fills).
 template <int AL>
-__device__ __forceinline__ int64_t nlm_tile_coord(int64_t gy, int64_t yi, int wx, int R, int64_t wp,
-                                                  int64_t x0, int64_t P, int64_t row_end) {
+__device__ __forceinline__ int2 nlm_tile_coord(int64_t gy, int64_t yi, int wx, int R, int64_t wp,
+                                               int64_t x0, int64_t row_end) {
     const int64_t dy = gy - yi;
-    if (yi >= row_end || dy < -R || dy > R || (dy == 0 && wx == 0)) return NLM_OOB;
-    const int64_t ad = dy < 0 ? -dy : dy;
-    const int64_t fi = ad == 0 ? -1 : R + (ad - 1) * (2 * R + 1) + R;  // fwd_index(|dy|, 0)
-    if (dy > 0 || (dy == 0 && wx > 0)) return (fi + wx) * P + yi * wp + x0;  // forward: at i
-    return (fi - wx) * P + gy * wp + x0 + wx - nlm_mis<AL>(wx);              // backward: at j
+    if (yi >= row_end || dy < -R || dy > R || (dy == 0 && wx == 0)) return make_int2(0, NLM_OOB);
+    const int ad = (int)(dy < 0 ? -dy : dy);
+    const int fi = ad == 0 ? -1 : R + (ad - 1) * (2 * R + 1) + R;  // fwd_index(|dy|, 0)
+    if (dy > 0 || (dy == 0 && wx > 0)) return make_int2((int)(yi * wp + x0), fi + wx);  // forward: at i
+    return make_int2((int)(gy * wp + x0 + wx - nlm_mis<AL>(wx)), fi - wx);           // backward: at j
 }
 
 template <typename WT>
@@ -1748,7 +1749,6 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ C
     constexpr int ZREC = NLM_ZW * NlmRec<S>::n;  // one staged row
 
     const int64_t wp = weight_pitch<WT>(width);
-    const int64_t P = slab_rows * wp;  // weight-plane stride
     const int64_t x0 = (int64_t)blockIdx.x * COLS;
     const int tx = threadIdx.x;
     const int64_t x = x0 + tx;
@@ -1782,8 +1782,8 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ C
                     tma_load_2d(wst + (size_t)st * SW + (size_t)t * NLM_TX, pmap2, c0, c1, &bar[st]);
                 }
             } else {
-                const int64_t c = nlm_tile_coord<AL>(gy, yi, wx, R, wp, x0, P, row_end);
-                tma_load_1d(wst + (size_t)st * SW + (size_t)t * NLM_TX, pmap, (int)c, &bar[st]);
+                const int2 c = nlm_tile_coord<AL>(gy, yi, wx, R, wp, x0, row_end);
+                tma_load_2d(wst + (size_t)st * SW + (size_t)t * NLM_TX, pmap, c.x, c.y, &bar[st]);
             }
         }
     };
@@ -1888,27 +1888,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// 1-D tiled tensor map over the weight planes (fwd_count(R) * N elements),
-// box NLM_TX; false if the driver call is unavailable or refuses.
-template <typename WT>
-bool nlm_weight_map(CUtensorMap* m, const WT* wbuf, int64_t total) {
-    auto enc = tensor_map_encoder();
-    if (!enc) return false;
-    cuuint64_t dim[1] = {(cuuint64_t)total};
-    // (rank 1 has no strides, but the driver rejects a null array: measured,
-    // tools/micro/tmap_probe.cu)
-    cuuint64_t st[1] = {(cuuint64_t)total * sizeof(WT)};
-    cuuint32_t box[1] = {(cuuint32_t)NLM_TX};
-    cuuint32_t es[1] = {1};
-    CUresult r = enc(m, sizeof(WT) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1,
-                     (void*)wbuf, dim, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-// 2-D view (P x planes, row stride P) with a box of NLM_TX x rows: a forward
-// row's 2R + 1 consecutive planes in one transfer
+// 2-D view of the weight planes (P x planes, row stride P) with a box of
+// NLM_TX x rows: rows = 1 for single tiles, 2R + 1 for a forward row's
+// consecutive planes in one transfer.  False if the driver call is
+// unavailable or refuses.  (A 1-D map over the flattened buffer also works
+// but caps the buffer at 2^31 elements of 32-bit coordinates.)
 template <typename WT>
 bool nlm_weight_map2(CUtensorMap* m, const WT* wbuf, int64_t P, int planes, int rows) {
     auto enc = tensor_map_encoder();
@@ -1939,7 +1923,7 @@ int launch_nlm_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows,
     constexpr int NS = POLSAR_NLM_NS;
     CUtensorMap wmap, wmap2;
     const int64_t P = slab_rows * weight_pitch<WT>(width);
-    if (!nlm_weight_map<WT>(&wmap, wbuf, (int64_t)fwd_count(R) * P) ||
+    if (!nlm_weight_map2<WT>(&wmap, wbuf, P, fwd_count(R), 1) ||
         !nlm_weight_map2<WT>(&wmap2, wbuf, P, fwd_count(R), 2 * R + 1))
         return fail(POLSAR_ECUDA, "polsar_nlm_filter: cuTensorMapEncodeTiled failed");
     const size_t smem = nlm_smem_bytes<WT>(R, RB, NS, sizeof(S));
@@ -2096,9 +2080,9 @@ int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_row
     if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
     if (!z || !workspace || !out_z) return fail(POLSAR_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    // (the symmetric form's gather addresses the weight buffer with 32-bit TMA coordinates)
+    // (the symmetric form's gather addresses a weight plane with 32-bit TMA coordinates)
     if (radius >= 1 && radius <= V3_RMAX && !nlm_direct() && tensor_map_encoder() &&
-        (int64_t)fwd_count(radius) * slab_rows * (width + 4) + NLM_TX < ((int64_t)1 << 31) - 1) {
+        slab_rows * (width + 4) + 2 * NLM_TX < ((int64_t)1 << 31)) {
         switch (dtype) {
             case POLSAR_F32:
                 return launch_nlm_sym<float, double, float>(z, ld, width, slab_rows, out_row_begin,
