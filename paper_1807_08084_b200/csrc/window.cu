@@ -838,13 +838,17 @@ int window_variant() {
 // symmetric and det((Z_i+Z_j)/2) is), so each unordered pair is evaluated
 // once.  Pass 1 (k_window_fwd) computes, for every pixel i, the weights of its
 // 2R(R+1) "forward" neighbours j = i + delta (delta_y > 0, or delta_y = 0 and
-// delta_x > 0): their sum F_i, and each weight stored at wbuf[delta][i].
-// Pass 2 (k_window_bwd) adds, for every output pixel j, the stored weights of
-// its backward neighbours: W_j = 1 + F_j + sum_delta wbuf[delta][j - delta]
-// (d_jj = 0 contributes exactly 1).  Half the FP64 work of k_window_sum for
-// 1068 B/pixel of workspace traffic (fp32 weights, R = 11); every sum is in a
-// fixed order, so results are bit-reproducible and slab decompositions are
-// exact.
+// delta_x > 0) and their sum F_i.  Each weight must also reach W_j:
+//  * ACC form (default for the window and KL): added to j's backward sum in
+//    shared memory as an exact fixed-point integer (acc_add below); pass 2
+//    (k_window_bwd_acc) adds the <= 4 tile sums of each pixel.
+//  * plane form (NLM, whose gather reads the weights; POLSAR_WINDOW_PLANES=1):
+//    stored at wbuf[delta][i]; pass 2 (k_window_bwd) adds, for every output
+//    pixel j, W_j = 1 + F_j + sum_delta wbuf[delta][j - delta] (1068 B/pixel
+//    of workspace traffic at R = 11, fp32 weights).
+// d_jj = 0 contributes exactly 1.  Half the FP64 work of k_window_sum; every
+// sum is exact or in a fixed order, so results are bit-reproducible and slab
+// decompositions are exact.
 __host__ __device__ __forceinline__ int fwd_count(int R) { return 2 * R * (R + 1); }
 // Row pitch of the weight planes: width rounded up to 16 bytes, so every row
 // of every plane starts 16-byte aligned (the TMA tiles of the NLM gather need
