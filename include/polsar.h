@@ -113,6 +113,16 @@ int polsar_inv_det_blocks(const void* z, void* out, uint8_t* status, int64_t n, 
  * weights; the default window and KL kernels need ~40 B per pixel.) */
 size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radius, int dtype);
 
+/* polsar_window_workspace_bytes_for -- the same for one entry point:
+ * entry 0 polsar_window_distance, 1 polsar_nlm_filter, 2 polsar_window_kl
+ * (0 for an invalid entry or an unsupported dtype / radius).  A workspace of
+ * this size serves every call of that entry point with these sizes in this
+ * process.  The window and KL sums need ~40 B per pixel, so a UAVSAR-scale
+ * slab (4e8 pixels) fits where the NLM's weight planes (~1 KB per pixel)
+ * cannot. */
+size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t width, int radius,
+                                         int dtype);
+
 /* polsar_window_distance -- non-local-means search-window sum (the workload
  * of PAPER.md:77-80 [§I]; formula of BASELINE.json configs[4]):
  *   W_i = sum_{j in N(i)} exp(-d_ij / h),
@@ -126,7 +136,8 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radiu
  *               <= slab_rows); out receives (e - b) x width values, row-major.
  *   radius R (>= 0, <= 16; the paper's 23x23 window is R = 11), looks L (> 0),
  *               h (> 0).
- *   workspace : device, polsar_window_workspace_bytes(slab_rows, width, radius, dtype)
+ *   workspace : device, polsar_window_workspace_bytes_for(0, slab_rows, width, radius, dtype)
+ *               (or the all-entry-points polsar_window_workspace_bytes)
  *   dtype     : POLSAR_F32 (fp32 storage, fp64 pair determinant, fp32
  *               weight) or POLSAR_F64 (fp64 throughout), or the _PLAIN
  *               variants (storage precision throughout).
@@ -144,7 +155,7 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
  *   d_ij = L [ (tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i)) / 2 - 3 ],  W_i = sum_j exp(-d_ij / h).
  * Z^-1 of every slab pixel comes from Alg. 2 (K1's device function) in a
  * prepass; each pair is then two 9-term trace products in fp64.  Arguments,
- * workspace (polsar_window_workspace_bytes) and errors as
+ * workspace (polsar_window_workspace_bytes_for(2, ...)) and errors as
  * polsar_window_distance; radius <= 12; dtype POLSAR_F32 or POLSAR_F64
  * (POLSAR_F32_PLAIN returns ENOTSUP). */
 int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
@@ -159,7 +170,7 @@ int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows
  *   out_w  : device, (e - b) x width values of W, or NULL
  *   out_z  : device, 9 planes of (e - b) x width filtered pixels (packed
  *            field order), plane stride ld_out >= (e - b) * width.
- * Workspace: polsar_window_workspace_bytes(slab_rows, width, radius, dtype). */
+ * Workspace: polsar_window_workspace_bytes_for(1, slab_rows, width, radius, dtype). */
 int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
                       int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
                       double h, void* workspace, void* out_w, void* out_z, int64_t ld_out,

@@ -23,7 +23,7 @@ STATUS_OK, STATUS_SINGULAR, STATUS_NOT_PD = 0, 1, 2
 
 __all__ = [
     "polsar_inv_det", "polsar_inv_det_cholesky", "polsar_inv_det_blocks", "polsar_window_distance",
-    "polsar_nlm_filter", "nlm_filter", "polsar_window_kl", "window_kl", "polsar_window_workspace_bytes", "polsar_checksum", "polsar_inv_det_host",
+    "polsar_nlm_filter", "nlm_filter", "polsar_window_kl", "window_kl", "polsar_window_workspace_bytes", "polsar_window_workspace_bytes_for", "polsar_checksum", "polsar_inv_det_host",
     "polsar_host_chunk_pixels", "inv_det", "window_distance", "dtype_code", "PolsarError",
     "POLSAR_F32", "POLSAR_F64", "POLSAR_F32_PLAIN", "POLSAR_F64_PLAIN",
 ]
@@ -128,6 +128,13 @@ def polsar_window_workspace_bytes(slab_rows: int, width: int, radius: int, dtype
     return int(lib().polsar_window_workspace_bytes(slab_rows, width, radius, dtype))
 
 
+WINDOW, NLM, KL = 0, 1, 2  # entry points of polsar_window_workspace_bytes_for
+
+
+def polsar_window_workspace_bytes_for(entry: int, slab_rows: int, width: int, radius: int, dtype: int) -> int:
+    return int(lib().polsar_window_workspace_bytes_for(int(entry), slab_rows, width, radius, dtype))
+
+
 def polsar_window_distance(z, width, slab_rows, out_row_begin, out_row_end, radius, looks, h,
                            workspace, out, plain=False, stream=None):
     """Search-window sum W_i (BASELINE configs[4]) for slab rows
@@ -135,7 +142,7 @@ def polsar_window_distance(z, width, slab_rows, out_row_begin, out_row_end, radi
     _dev_check(z, workspace, out)
     ld = _planes(z, 9)
     code = dtype_code(z.dtype, plain)
-    need = polsar_window_workspace_bytes(slab_rows, width, radius, code)
+    need = polsar_window_workspace_bytes_for(WINDOW, slab_rows, width, radius, code)
     if workspace.numel() * workspace.element_size() < need:
         raise ValueError(f"workspace needs {need} bytes")
     if out.numel() < (out_row_end - out_row_begin) * width or out.dtype != z.dtype:
@@ -153,8 +160,8 @@ def window_distance(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, 
     torch = _torch()
     row_end = height if row_end is None else row_end
     code = dtype_code(z.dtype, plain)
-    ws = torch.empty(polsar_window_workspace_bytes(height, width, radius, code), dtype=torch.uint8,
-                     device=z.device)
+    ws = torch.empty(polsar_window_workspace_bytes_for(WINDOW, height, width, radius, code),
+                     dtype=torch.uint8, device=z.device)
     out = torch.empty((row_end - row_begin) * width, dtype=z.dtype, device=z.device)
     return polsar_window_distance(z, width, height, row_begin, row_end, radius, looks, h, ws, out,
                                   plain=plain, stream=stream)
@@ -166,7 +173,7 @@ def polsar_window_kl(z, width, slab_rows, out_row_begin, out_row_end, radius, lo
     _dev_check(z, workspace, out)
     ld = _planes(z, 9)
     code = dtype_code(z.dtype)
-    need = polsar_window_workspace_bytes(slab_rows, width, radius, code)
+    need = polsar_window_workspace_bytes_for(KL, slab_rows, width, radius, code)
     if workspace.numel() * workspace.element_size() < need:
         raise ValueError(f"workspace needs {need} bytes")
     if out.numel() < (out_row_end - out_row_begin) * width or out.dtype != z.dtype:
@@ -183,8 +190,8 @@ def window_kl(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, row_en
     torch = _torch()
     row_end = height if row_end is None else row_end
     code = dtype_code(z.dtype)
-    ws = torch.empty(polsar_window_workspace_bytes(height, width, radius, code), dtype=torch.uint8,
-                     device=z.device)
+    ws = torch.empty(max(1, polsar_window_workspace_bytes_for(KL, height, width, radius, code)),
+                     dtype=torch.uint8, device=z.device)
     out = torch.empty((row_end - row_begin) * width, dtype=z.dtype, device=z.device)
     return polsar_window_kl(z, width, height, row_begin, row_end, radius, looks, h, ws, out,
                             stream=stream)
@@ -198,7 +205,7 @@ def polsar_nlm_filter(z, width, slab_rows, out_row_begin, out_row_end, radius, l
     ld = _planes(z, 9)
     ld_out = _planes(out_z, 9)
     code = dtype_code(z.dtype, plain)
-    need = polsar_window_workspace_bytes(slab_rows, width, radius, code)
+    need = polsar_window_workspace_bytes_for(NLM, slab_rows, width, radius, code)
     if workspace.numel() * workspace.element_size() < need:
         raise ValueError(f"workspace needs {need} bytes")
     if out_z.dtype != z.dtype or (out_w is not None and out_w.dtype != z.dtype):
@@ -217,8 +224,8 @@ def nlm_filter(z, height, width, radius=11, looks=4.0, h=1.0, row_begin=0, row_e
     row_end = height if row_end is None else row_end
     m = (row_end - row_begin) * width
     code = dtype_code(z.dtype, plain)
-    ws = torch.empty(polsar_window_workspace_bytes(height, width, radius, code), dtype=torch.uint8,
-                     device=z.device)
+    ws = torch.empty(polsar_window_workspace_bytes_for(NLM, height, width, radius, code),
+                     dtype=torch.uint8, device=z.device)
     out_z = torch.empty((9, m), dtype=z.dtype, device=z.device)
     out_w = torch.empty(m, dtype=z.dtype, device=z.device)
     polsar_nlm_filter(z, width, height, row_begin, row_end, radius, looks, h, ws, out_z, out_w,

@@ -25,6 +25,7 @@ SIGNATURES = {
     "polsar_inv_det_cholesky": (INT, [P, P, U8P, I64, I64, INT, P]),
     "polsar_inv_det_blocks": (INT, [P, P, U8P, I64, I64, INT, INT, P]),
     "polsar_window_workspace_bytes": (SZ, [I64, I64, INT, INT]),
+    "polsar_window_workspace_bytes_for": (SZ, [INT, I64, I64, INT, INT]),
     "polsar_window_distance": (INT, [P, I64, I64, I64, I64, I64, INT, D, D, P, P, INT, P]),
     "polsar_window_kl": (INT, [P, I64, I64, I64, I64, I64, INT, D, D, P, P, INT, P]),
     "polsar_nlm_filter": (INT, [P, I64, I64, I64, I64, I64, INT, D, D, P, P, P, I64, INT, P]),

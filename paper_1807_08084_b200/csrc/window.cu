@@ -1969,28 +1969,52 @@ using namespace polsar_impl;
 
 extern "C" {
 
-size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radius, int dtype) {
-    if (slab_rows < 0 || width < 0 || radius < 0) return 0;
+size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t width, int radius,
+                                         int dtype) {
+    if (slab_rows < 0 || width < 0 || radius < 0 || entry < 0 || entry > 2) return 0;
     const int64_t n = slab_rows * width;
     const bool wt64 = dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN;
-    // the largest need of the kernels the call may run: direct form / NLM
-    // (one plane of g), the expansion form and KL (20 fp64 planes), the
-    // symmetric form (g, F and 2R(R+1) weight planes)
-    size_t b = (((size_t)n * (wt64 ? 8 : 4)) + 255) / 256 * 256;
-    if (dtype != POLSAR_F32_PLAIN) b = std::max(b, ((size_t)n * 160 + 255) / 256 * 256);
-    if (radius <= V3_RMAX) {
-        b = std::max(b, wt64 ? window_sym_bytes<double>(slab_rows, width, radius)
-                             : window_sym_bytes<float>(slab_rows, width, radius));
-        b = std::max(b, acc_sym_bytes((size_t)n * (wt64 ? 8 : 4), slab_rows, width, radius, POLSAR_SYM_TY));
-        if (dtype != POLSAR_F32_PLAIN) {
-            b = std::max(b, acc_sym_bytes((size_t)n * V3_NP * sizeof(double), slab_rows, width, radius, 16));
-            b = std::max(b, acc_sym_bytes((size_t)n * V3_NP * sizeof(double), slab_rows, width, radius,
-                                          POLSAR_KLF_TY));
+    const size_t wt = wt64 ? 8 : 4;
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    const bool sym_ok = radius <= V3_RMAX;
+    const int v = window_variant();
+    // the largest need of the kernels this entry point may run (with this
+    // process's POLSAR_* A/B settings, which the library reads the same way)
+    size_t b = up((size_t)n * wt);  // direct forms: one plane of g
+    if (entry == 0) {                // polsar_window_distance
+        if (sym_ok && v == 3 && dtype != POLSAR_F32_PLAIN) b = std::max(b, up((size_t)n * 160));
+        if (sym_ok && v == 4) {
+            b = std::max(b, acc_sym_bytes((size_t)n * wt, slab_rows, width, radius, POLSAR_SYM_TY));
+            if (window_planes())
+                b = std::max(b, wt64 ? window_sym_bytes<double>(slab_rows, width, radius)
+                                     : window_sym_bytes<float>(slab_rows, width, radius));
         }
-        if (dtype != POLSAR_F32_PLAIN)
-            b = std::max(b, wt64 ? kl_sym_bytes<double>(slab_rows, width, radius)
-                                 : kl_sym_bytes<float>(slab_rows, width, radius));
+    } else if (entry == 1) {         // polsar_nlm_filter (the dispatch conditions of the gather form)
+        if (sym_ok && radius >= 1 && !nlm_direct() && slab_rows * (width + 4) + 2 * NLM_TX < ((int64_t)1 << 31))
+            b = std::max(b, wt64 ? window_sym_bytes<double>(slab_rows, width, radius)
+                                 : window_sym_bytes<float>(slab_rows, width, radius));
+    } else {                         // polsar_window_kl (radius <= 12; no fp32-arithmetic mode)
+        if (dtype == POLSAR_F32_PLAIN || !sym_ok) return 0;
+        b = std::max(b, up((size_t)n * 160));  // prepass planes (the streaming form's too)
+        if (v == 4) {  // the choice of launch_window_kl_sym
+            const size_t pre = (size_t)n * V3_NP * sizeof(double);
+            const bool planes = window_planes();
+            if (!wt64 && !planes && acc_fwd_smem<KLPairF<float>>(POLSAR_KLF_TY, radius) <= K3_SMEM_MAX)
+                b = std::max(b, acc_sym_bytes(pre, slab_rows, width, radius, POLSAR_KLF_TY));
+            else if (!planes && acc_fwd_smem<KLPair<float>>(16, radius) <= K3_SMEM_MAX)
+                b = std::max(b, acc_sym_bytes(pre, slab_rows, width, radius, 16));
+            else  // the weight-plane form (POLSAR_WINDOW_PLANES=1, or R = 12)
+                b = std::max(b, wt64 ? kl_sym_bytes<double>(slab_rows, width, radius)
+                                     : kl_sym_bytes<float>(slab_rows, width, radius));
+        }
     }
+    return b;
+}
+
+size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radius, int dtype) {
+    size_t b = 0;
+    for (int e = 0; e < 3; ++e)
+        b = std::max(b, polsar_window_workspace_bytes_for(e, slab_rows, width, radius, dtype));
     return b;
 }
 

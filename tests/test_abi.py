@@ -92,19 +92,29 @@ def test_product_never_imports_oracle():
 @pytest.mark.parametrize("rows,width,radius", [(1, 1, 11), (1, 50, 4), (5, 300, 12), (130, 7, 1),
                                                (2048, 2048, 11), (37, 53, 3), (3, 3, 0)])
 def test_window_workspace_covers_every_form(rows, width, radius):
-    """polsar_window_workspace_bytes >= the need of every form a window call
-    may run: the weight planes (pitch rounded to 16 bytes), the
-    tiles' backward sums of the shared-memory form (32-column tiles of 32 rows,
-    or 16 / 24 for KL, each (32 + 2R)(TY + R) int64), and the KL prepass."""
+    """polsar_window_workspace_bytes_for(entry) >= the need of every form that
+    entry point may run: the weight planes (pitch rounded to 16
+    bytes) for the NLM, the tiles' backward sums of the shared-memory form
+    (32-column tiles of 32 rows, or 24 / 16 for KL, each (32 + 2R)(TY + R)
+    int64) and the KL prepass; polsar_window_workspace_bytes >= all of them."""
     lib = _lib.lib()
     up = lambda b: (b + 255) // 256 * 256  # noqa: E731
     n = rows * width
     for dtype, wt in ((0, 4), (1, 8), (2, 4), (3, 8)):
-        got = lib.polsar_window_workspace_bytes(rows, width, radius, dtype)
         pitch = (width + 16 // wt - 1) // (16 // wt) * (16 // wt)
-        need = [up(n * wt) + up(n * 8) + up(2 * radius * (radius + 1) * rows * pitch * wt)]
-        kl = [] if dtype == 2 else [(16, n * 160), (24, n * 160)]  # (no KL in POLSAR_F32_PLAIN)
-        for ty, pre in [(32, n * wt)] + kl:
+        planes = up(n * wt) + up(n * 8) + up(2 * radius * (radius + 1) * rows * pitch * wt)
+
+        def acc(pre, ty):
             tiles = ((width + 31) // 32) * ((rows + ty - 1) // ty)
-            need.append(up(pre) + up(n * 8) + up(tiles * (32 + 2 * radius) * (ty + radius) * 8))
-        assert got >= max(need), (dtype, got, need)
+            return up(pre) + up(n * 8) + up(tiles * (32 + 2 * radius) * (ty + radius) * 8)
+        need = {0: [up(n * wt), acc(n * wt, 32)], 1: [up(n * wt)] + ([planes] if radius >= 1 else []), 2: []}
+        if dtype != 2:  # (no KL in POLSAR_F32_PLAIN)
+            need[2] = [up(n * 160), acc(n * 160, 24 if wt == 4 else 16)]
+            if radius == 12:
+                need[2].append(planes - up(n * wt) + up(n * 160))  # KL's plane form at R = 12
+        for e in range(3):
+            got = lib.polsar_window_workspace_bytes_for(e, rows, width, radius, dtype)
+            assert got >= max(need[e], default=0), (e, dtype, got, need[e])
+            assert lib.polsar_window_workspace_bytes(rows, width, radius, dtype) >= got
+        if dtype == 0 and rows * width > 1000 and radius >= 8:  # the window sum needs far less than the NLM
+            assert 8 * lib.polsar_window_workspace_bytes_for(0, rows, width, radius, dtype) < planes

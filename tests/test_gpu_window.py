@@ -145,3 +145,28 @@ def test_window_nonfinite_input_propagates(cuda, fn):
     near = (np.abs(ys - yb) <= r) & (np.abs(xs - xb) <= r)
     assert np.all(np.isnan(got[near]))
     assert np.all(np.isfinite(got[~near]))
+
+
+@pytest.mark.parametrize("entry,radius,shape", [(0, 11, (150, 300)), (0, 12, (60, 100)), (0, 14, (40, 45)),
+                                                (1, 11, (150, 300)), (1, 3, (37, 53)),
+                                                (2, 11, (150, 300)), (2, 12, (60, 100))])
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_workspace_for_entry_is_enough(cuda, entry, radius, shape, dt):
+    """A workspace of exactly polsar_window_workspace_bytes_for(entry) bytes:
+    the call succeeds and the 64 KB canary after it is untouched."""
+    h, w = shape
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda).to(dt)
+    code = P.dtype_code(dt)
+    need = P.polsar_window_workspace_bytes_for(entry, h, w, radius, code)
+    buf = torch.full((need + 65536,), 0xAB, dtype=torch.uint8, device=cuda)
+    ws = buf[:need]
+    out = torch.empty(h * w, dtype=dt, device=cuda)
+    if entry == 0:
+        P.polsar_window_distance(z, w, h, 0, h, radius, 4.0, 1.0, ws, out)
+    elif entry == 1:
+        P.polsar_nlm_filter(z, w, h, 0, h, radius, 4.0, 1.0, ws, torch.empty((9, h * w), dtype=dt, device=cuda), out)
+    else:
+        P.polsar_window_kl(z, w, h, 0, h, radius, 4.0, 1.0, ws, out)
+    torch.cuda.synchronize()
+    assert bool((buf[need:] == 0xAB).all())
+    assert bool(torch.isfinite(out).all()) and float(out.min()) >= 1 - 1e-6
