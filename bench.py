@@ -317,8 +317,8 @@ def run_ours(args):
         "clocks": sampler.summary(),
         "gpu_launches": args.steps,
         "checksum": f"{checksum:016x}", "status_counts": counts,
-        "t_step_ms": {"min": min(per_step_ms), "avg": sum(per_step_ms) / len(per_step_ms),
-                      "max": max(per_step_ms)},
+        "t_step_ms": {"min": min(per_step_ms), "avg": float(np.mean(per_step_ms)),
+                      "max": max(per_step_ms), "std": float(np.std(per_step_ms))},
     }
 
     # ---------------- e2e: the public host-buffer entry point, copies inside
