@@ -408,6 +408,26 @@ def _time_kernel(torch, stream, fn, steps, warm=3):
     return a.elapsed_time(b) / 1e3 / steps
 
 
+def _time_kernel_flushed(torch, stream, fn, steps, flush, warm=3):
+    """Mean per-launch time with the L2 flushed (a 512 MB fill) before every
+    launch; only the launch is inside the events."""
+    for _ in range(warm):
+        fn()
+    stream.synchronize()
+    ts = []
+    for i in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xFF)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        ts.append((a, b))
+    stream.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ts) / 1e3 / steps
+
+
 def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
     from paper_1807_08084_b200 import configs, wishart
     n = z.shape[1]
@@ -421,6 +441,23 @@ def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
             gbs = n * bpm / t / 1e9
             res[f"{algo}{'_plain' if plain else ''}"] = {
                 "matrices_per_s": n / t, "ms": t * 1e3, "GB/s": gbs, "frac_hbm": gbs / peak}
+    # BASELINE configs[1] (c2: 1024^2 fp32, 4 quadrant classes), the paper-scale
+    # head-to-head of both kernels; 84 MB fits the 126 MB L2, so it is flushed
+    # before every launch (launch-latency bound: ~13 us at the HBM roof)
+    c2 = configs.get("c2")
+    with torch.cuda.stream(stream):
+        z2 = wishart.generate(c2, device=dev)
+        o2 = torch.empty((11, c2.n), dtype=z2.dtype, device=dev)
+        s2 = torch.empty(c2.n, dtype=torch.uint8, device=dev)
+        flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)
+    stream.synchronize()
+    for algo, fn in (("adjugate", P.polsar_inv_det), ("cholesky", P.polsar_inv_det_cholesky)):
+        t = _time_kernel_flushed(torch, stream, lambda: fn(z2, o2, s2, stream=stream), steps, flush)
+        gbs = c2.n * 81 / t / 1e9
+        res[f"c2_{algo}"] = {"matrices_per_s": c2.n / t, "ms": t * 1e3, "GB/s": gbs, "frac_hbm": gbs / peak,
+                             "mode": "fp32 storage, L2 flushed before each launch"}
+    del z2, o2, s2, flush
+    torch.cuda.empty_cache()
     # K1 on BASELINE configs[3] (c4: 4e8 px fp64 storage, error-free Alg. 2),
     # 161 B / matrix
     c4 = configs.get("c4")
