@@ -269,7 +269,7 @@ def run_ours(args):
         for i in range(args.steps):
             if l2_flush is not None:
                 with torch.cuda.stream(stream):
-                    l2_flush.fill_(i & 0xFF)
+                    l2_flush.sum(dtype=torch.int64)  # a 512 MB read: clean lines, no write-back tail
             starts[i].record(stream)
             step()
             ends[i].record(stream)
@@ -409,7 +409,7 @@ def _time_kernel(torch, stream, fn, steps, warm=3):
 
 
 def _time_kernel_flushed(torch, stream, fn, steps, flush, warm=3):
-    """Mean per-launch time with the L2 flushed (a 512 MB fill) before every
+    """Mean per-launch time with the L2 flushed (a 512 MB read) before every
     launch; only the launch is inside the events."""
     for _ in range(warm):
         fn()
@@ -417,7 +417,7 @@ def _time_kernel_flushed(torch, stream, fn, steps, flush, warm=3):
     ts = []
     for i in range(steps):
         with torch.cuda.stream(stream):
-            flush.fill_(i & 0xFF)
+            flush.sum(dtype=torch.int64)  # read 512 MB: evicts with clean lines, no write-back tail
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
