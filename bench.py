@@ -543,9 +543,15 @@ def measure_cpu_baseline(z, cfg):
     t0 = time.perf_counter()
     oracle.inv_det_threaded(zs, cores)
     t = time.perf_counter() - t0
+    # the same oracle on one core, on a ~2 s sample
+    one = int(min(sample, max(1 << 16, rate / cores * 2.0)))
+    t1 = time.perf_counter()
+    oracle.inv_det_threaded(zs[:, :one], 1)
+    t1 = time.perf_counter() - t1
     return {"value": sample / t, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"first {sample} pixels of this rank's {cfg.name} input (D2H copy), "
-                      f"{t:.1f} s wall on {cores} threads"}
+                      f"{t:.1f} s wall on {cores} threads",
+            "single_core": {"value": one / t1, "sample": f"first {one} pixels, {t1:.1f} s on 1 thread"}}
 
 
 def verify_sample(P, z, out, status, cfg, r0):
