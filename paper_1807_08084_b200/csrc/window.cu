@@ -87,8 +87,20 @@ __device__ __forceinline__ float pair_weight(float r, float alpha, bool alpha_is
     if (alpha_is_2) return fast_rcp(r * r);
     return fast_exp2(-alpha * fast_log2(r));
 }
+// 1/x for the fp64 weight: MUFU's ~23-bit reciprocal and two Newton steps
+// (error squared each step: <= 2 ulp), against div.rn.f64's longer sequence
+// with its special-case branch.  x = r^2 > 0 and finite for valid pixels; a
+// NaN or 0 propagates as NaN / inf (the NaN marks of R-19 survive).
+__device__ __forceinline__ double fast_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = __fma_rn(-x, y, 1.0);
+    y = __fma_rn(y, e, y);
+    e = __fma_rn(-x, y, 1.0);
+    return __fma_rn(y, e, y);
+}
 __device__ __forceinline__ double pair_weight(double r, double alpha, bool alpha_is_2) {
-    if (alpha_is_2) return 1.0 / (r * r);
+    if (alpha_is_2) return fast_rcp(r * r);
     return exp(-alpha * log(r));
 }
 
