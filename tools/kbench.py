@@ -65,6 +65,13 @@ def main():
             res["kl_c5_ms"] = timeit(lambda: P.polsar_window_kl(z, c5.width, c5.height, 0, c5.height,
                                                                 c5.radius, c5.looks, c5.h, ws32, wo,
                                                                 stream=s), s, steps=3)
+            res["kl_c5_fp64_ms"] = timeit(lambda: P.polsar_window_kl(z64, c5.width, c5.height, 0, c5.height,
+                                                                     c5.radius, c5.looks, c5.h, ws, out,
+                                                                     stream=s), s, steps=3)
+            zz64 = torch.empty((9, c5.n), dtype=torch.float64, device=dev)
+            res["nlm_c5_fp64_ms"] = timeit(lambda: P.polsar_nlm_filter(z64, c5.width, c5.height, 0, c5.height,
+                                                                       c5.radius, c5.looks, c5.h, ws, zz64, out,
+                                                                       stream=s), s, steps=3)
             res["window_c5_fp64_ms"] = timeit(lambda: P.polsar_window_distance(
                 z64, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, out,
                 stream=s), s, steps=3)
