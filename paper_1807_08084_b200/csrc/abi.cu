@@ -25,16 +25,14 @@ int launch_check(const char* what) {
     return POLSAR_OK;
 }
 
-static int g_num_sms = 0;
-
-int num_sms() {
-    if (!g_num_sms) {
-        int dev = 0;
+int num_sms() {  // of the device current at first use (read once, thread-safe)
+    static const int n = [] {
+        int dev = 0, v = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    return g_num_sms;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    return n;
 }
 
 // one thread per work item, the whole batch in one grid (capped at 2^31-1

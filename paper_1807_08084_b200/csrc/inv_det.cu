@@ -226,12 +226,11 @@ k_inv_det_bulk(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict
     if (tid == 0) bulk_wait<0>();
 }
 
-int k1_variant() {
-    static int v = -1;
-    if (v < 0) {
+int k1_variant() {  // (read once; thread-safe static initialisation)
+    static const int v = [] {
         const char* e = getenv("POLSAR_K1_VARIANT");
-        v = (e && e[0] == 'b') ? 1 : 0;
-    }
+        return (e && e[0] == 'b') ? 1 : 0;
+    }();
     return v;
 }
 

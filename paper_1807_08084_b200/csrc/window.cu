@@ -836,12 +836,12 @@ int launch_window_kl(const void* zv, int64_t ld, int64_t width, int64_t slab_row
 // Eq. 6 on S = Z_i + Z_j for every ordered pair), 3 (cubic expansion over
 // per-pixel adjugates).  POLSAR_WINDOW_VARIANT=2|3 selects the alternatives
 // for A/B runs; all are parity-tested.  R > 12 always runs variant 2.
+// (read once; function-local static initialisation is thread-safe)
 int window_variant() {
-    static int v = -1;
-    if (v < 0) {
+    static const int v = [] {
         const char* e = getenv("POLSAR_WINDOW_VARIANT");
-        v = (e && (e[0] == '2' || e[0] == '3')) ? e[0] - '0' : 4;
-    }
+        return (e && (e[0] == '2' || e[0] == '3')) ? e[0] - '0' : 4;
+    }();
     return v;
 }
 
@@ -1447,12 +1447,11 @@ inline size_t acc_sym_bytes(size_t pre_bytes, int64_t slab_rows, int64_t width, 
 // Window / KL symmetric form: backward sums in shared memory (ACC, default)
 // or through the weight planes (POLSAR_WINDOW_PLANES=1, the A/B alternative).
 bool window_planes() {
-    static int v = -1;
-    if (v < 0) {
+    static const bool v = [] {
         const char* e = getenv("POLSAR_WINDOW_PLANES");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
+        return e && e[0] == '1';
+    }();
+    return v;
 }
 
 template <typename S, typename WT>
@@ -1891,16 +1890,14 @@ k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ C
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-    }
+        return (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                   ? (PFN_cuTensorMapEncodeTiled_v12000)p
+                   : nullptr;
+    }();
     return fn;
 }
 
@@ -1966,12 +1963,11 @@ int launch_nlm_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows,
 // NLM variant: symmetric (pass 1 + gather, default for R <= V3_RMAX) or the
 // direct form (POLSAR_NLM_VARIANT=direct, and always for R > V3_RMAX).
 bool nlm_direct() {
-    static int v = -1;
-    if (v < 0) {
+    static const bool v = [] {
         const char* e = getenv("POLSAR_NLM_VARIANT");
-        v = (e && e[0] == 'd') ? 1 : 0;
-    }
-    return v == 1;
+        return e && e[0] == 'd';
+    }();
+    return v;
 }
 
 }  // namespace
