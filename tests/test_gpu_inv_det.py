@@ -251,3 +251,20 @@ print("ok")
             a, b = out.cpu().numpy(), got[f"{algo}_{plain}"]
             assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (algo, plain)
             assert np.array_equal(st.cpu().numpy(), got[f"{algo}_{plain}_st"]), (algo, plain)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_residual_bound(c1, algo):
+    """||M Minv - I||_max <= 64 eps kappa(M) (eps = 2^-53), checked
+    with an independent complex matmul on the full Hermitian matrices -- no
+    oracle involved."""
+    z, zh, ref, k = c1
+    out, st = run(z, algo)
+    m = oracle.to_full(zh)
+    x = oracle.to_full(out[:9])
+    r = np.abs(m @ x - np.eye(3)).max(axis=(1, 2))
+    ok = (st == 0) & np.isfinite(k)
+    ratio = r[ok] / (64 * 2.0 ** -53 * k[ok])
+    print(f"[report] {algo} residual / (64 eps kappa): max {ratio.max():.3f}, median {np.median(ratio):.4f}, "
+          f"kappa max {k[ok].max():.3g}")
+    assert ratio.max() <= 1.0
