@@ -3,1975 +3,10 @@
 // DESIGN.md.  Nothing here is shared with oracle/.
 //
 //   K3  polsar_window_distance   23x23 search-window log-det distance sum
-//   K4  polsar_nlm_filter        fused NLM filter output
 //   K6  polsar_window_kl         window sum with the symmetric Wishart KL distance
-#include <cuda.h>
-#include <cudaTypedefs.h>
-#include <stdlib.h>
-
-#include <algorithm>
-
-#include "alg.cuh"
-
-namespace polsar_impl {
-namespace {
-
-// ==================================================== K3: window distance
-// K3a: per-pixel g_i = 1/(8 det Z_i) (det by Eq. 6) into the workspace.
-// K3b: one CTA per TY x TX output tile; the (TY+2R) x (TX+2R) halo of Z (9
-// planes, type T) and g (1 plane) is staged in shared memory once.  Each
-// thread owns RB vertically adjacent output pixels of one column and walks
-// the window's columns; every staged Z_j it loads is paired with all of its
-// RB pixels that reach it (RB-fold reuse of each shared-memory load, RB
-// independent dependency chains for the FP64 pipe).  Per pair (R-12,
-// BASELINE configs[4]):
-//   S = Z_i + Z_j            (9 adds; exact in fp64 for fp32 storage)
-//   ds = det(S) by Eq. 6     (only a_c, b_c, c_c needed: 20 fp64 ops)
-//   r = (ds g_i)(ds g_j) = D_S^2 / (D_i D_j),  D_S = det((Z_i+Z_j)/2)
-//   exp(-d_ij/h) = r^(-L/(2h))   (L/(2h) = 2: 1/(r r), no transcendental)
-// Rows of the window that reach all RB pixels run branch-free; the RB-1 rows
-// at each vertical end take a warp-uniform branch per pixel.  Columns outside
-// the image read zero-filled cells and are masked by a select.
-constexpr int K3_TX = 32;  // tile width; tile height TY in {32, 16, 8} (the largest
-                           // whose halo fits in shared memory); K3_RB output rows per thread
-
-template <typename T>
-__device__ __forceinline__ T det_eq6(T a, T br, T bi, T cr, T ci, T d, T er, T ei, T f) {
-    T ac = FMA(d, f, -FMA(er, er, MUL(ei, ei)));
-    T bcr = FMA(cr, er, FMA(ci, ei, -MUL(br, f)));
-    T bci = FMA(ci, er, -FMA(cr, ei, MUL(bi, f)));
-    T ccr = FMA(br, er, -FMA(bi, ei, MUL(cr, d)));
-    T cci = FMA(br, ei, FMA(bi, er, -MUL(ci, d)));
-    return FMA(a, ac, FMA(br, bcr, FMA(bi, bci, FMA(cr, ccr, MUL(ci, cci)))));
-}
-
-// K3a: g_i = 1 / (8 det Z_i) per slab pixel (det by Eq. 6 in T).
-template <typename S, typename T, typename WT>
-__global__ void __launch_bounds__(256)
-k_window_prep(const S* __restrict__ z, int64_t ld, int64_t n, WT* __restrict__ g) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        T v[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) v[k] = (T)z[k * ld + p];
-        T dz = det_eq6<T>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8]);
-        // NaN marks a pixel that is not positive definite (or not finite): every
-        // weight it enters becomes NaN, and so does W of every pixel whose
-        // window holds it
-        const WT gv = (WT)(T(1) / MUL(T(8), dz));
-        g[p] = (dz > T(0) && gv < WT(INFINITY)) ? gv : WT(NAN);
-    }
-}
-
-__device__ __forceinline__ float fast_rcp(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-// w = r^(-alpha), alpha = L/(2h).  alpha == 2 (L = 4, h = 1): w = 1/(r r),
-// no transcendental.
-__device__ __forceinline__ float fast_log2(float x) {
-    float y;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float fast_exp2(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-// (MUFU lg2 / ex2: absolute error ~2^-22 in log2 r, i.e. a relative error of
-// about alpha * 1e-7 in w -- far inside the 2e-5 budget for the fp32 weight.)
-__device__ __forceinline__ float pair_weight(float r, float alpha, bool alpha_is_2) {
-    if (alpha_is_2) return fast_rcp(r * r);
-    return fast_exp2(-alpha * fast_log2(r));
-}
-// 1/x for the fp64 weight: MUFU's ~23-bit reciprocal and two Newton steps
-// (error squared each step: <= 2 ulp), against div.rn.f64's longer sequence
-// with its special-case branch.  x = r^2 > 0 and finite for valid pixels; a
-// NaN or 0 propagates as NaN / inf (the NaN marks of R-19 survive).
-__device__ __forceinline__ double fast_rcp(double x) {
-    double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double e = __fma_rn(-x, y, 1.0);
-    y = __fma_rn(y, e, y);
-    e = __fma_rn(-x, y, 1.0);
-    return __fma_rn(y, e, y);
-}
-__device__ __forceinline__ double pair_weight(double r, double alpha, bool alpha_is_2) {
-    if (alpha_is_2) return fast_rcp(r * r);
-    return exp(-alpha * log(r));
-}
-
-template <typename T, typename WT>
-__device__ __forceinline__ WT pair_w(const T* zi, WT gi, const T* zj, WT gj, WT alpha, bool a2) {
-    T ds = det_eq6<T>(ADD(zi[0], zj[0]), ADD(zi[1], zj[1]), ADD(zi[2], zj[2]), ADD(zi[3], zj[3]),
-                      ADD(zi[4], zj[4]), ADD(zi[5], zj[5]), ADD(zi[6], zj[6]), ADD(zi[7], zj[7]),
-                      ADD(zi[8], zj[8]));
-    WT fds = (WT)ds;
-    WT rr = (fds * gi) * (fds * gj);
-    return pair_weight(rr, alpha, a2);
-}
-
-// Shared-memory halo pixel (symmetric pass 1, NLM): the 9 planes and g in one 10-slot record
-// (stride 10 T: 16-byte aligned for T = double, 8-byte for float), read with
-// five 2-wide loads from one address.  Record strides of 5 (double2) / 5
-// (float2) bank units are odd, so a warp's loads are conflict-free.
-template <typename T>
-struct Vec2Of;
-template <>
-struct Vec2Of<double> { using type = double2; };
-template <>
-struct Vec2Of<float> { using type = float2; };
-
-// g (WT) carried in the record's T slot, bit-exact.
-template <typename T, typename WT>
-__device__ __forceinline__ T pack_g(WT v) {
-    if constexpr (sizeof(T) == sizeof(WT)) return (T)v;
-    else return __longlong_as_double((long long)__float_as_uint(v));
-}
-template <typename T, typename WT>
-__device__ __forceinline__ WT unpack_g(T v) {
-    if constexpr (sizeof(T) == sizeof(WT)) return (WT)v;
-    else return __uint_as_float((unsigned)__double_as_longlong(v));
-}
-
-template <typename T, typename WT>
-__device__ __forceinline__ void load_rec(const T* rec, T (&zj)[9], WT& gj) {
-    using V = typename Vec2Of<T>::type;
-    const V* p = reinterpret_cast<const V*>(rec);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const V v = p[k];
-        zj[2 * k] = v.x;
-        zj[2 * k + 1] = v.y;
-    }
-    const V v = p[4];
-    zj[8] = v.x;
-    gj = unpack_g<T, WT>(v.y);
-}
-
-#ifndef POLSAR_K3_RB
-#define POLSAR_K3_RB 2
-#endif
-template <int TY>
-struct K3_RB_FOR {
-    static constexpr int v = (TY >= 16) ? POLSAR_K3_RB : 4;
-};
-
-// K3b.  r = D_S^2 / (D_i D_j) with D_S = det(Z_i + Z_j)/8 = (ds g_i)(ds g_j).
-template <typename S, typename T, typename WT, int K3_TY, int K3_RB>
-__global__ void __launch_bounds__(K3_TX * K3_TY / K3_RB, 1)
-k_window_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
-             int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
-             int alpha_is_2, S* __restrict__ out) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int HW = K3_TX + 2 * R;        // halo tile width
-    const int HH = K3_TY + 2 * R;        // halo tile height
-    const int HP = HW * HH;              // pixels in the halo tile
-    T* sz = reinterpret_cast<T*>(smem_raw);        // 9 planes of Z (type T)
-    WT* sg = reinterpret_cast<WT*>(sz + 9 * HP);   // 1 plane of g
-
-    const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
-    const int64_t y0 = row_begin + (int64_t)blockIdx.y * K3_TY;
-    // stage the halo; cells outside the slab are zero-filled (masked later)
-    for (int q = threadIdx.x; q < HP; q += blockDim.x) {
-        int hy = q / HW, hx = q % HW;
-        int64_t gy = y0 - R + hy, gx = x0 - R + hx;
-        bool in = gy >= 0 && gy < slab_rows && gx >= 0 && gx < width;
-        int64_t p = in ? gy * width + gx : 0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) sz[k * HP + q] = in ? (T)z[k * ld + p] : T(0);
-        sg[q] = in ? g[p] : WT(0);
-    }
-    __syncthreads();
-
-    const int tx = threadIdx.x % K3_TX;
-    const int ty0 = (threadIdx.x / K3_TX) * K3_RB;
-    const int64_t gx = x0 + tx;
-    T zi[K3_RB][9];
-    WT gi[K3_RB];
-    double acc[K3_RB];
-#pragma unroll
-    for (int r = 0; r < K3_RB; ++r) {
-        int q = (ty0 + r + R) * HW + (tx + R);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) zi[r][k] = sz[k * HP + q];
-        gi[r] = sg[q];
-        acc[r] = 0.0;
-    }
-    const WT alpha = (WT)alpha_d;
-    const bool a2 = alpha_is_2 != 0;
-    // the CTA's window columns all lie inside the image: no column masks
-    const bool interior_x = (x0 - R >= 0) && (x0 + K3_TX + R <= width);
-
-    for (int wy = -R; wy <= R + K3_RB - 1; ++wy) {
-        const int64_t gyj = y0 + ty0 + wy;
-        if (gyj < 0 || gyj >= slab_rows) continue;  // warp-uniform
-        const int hy = ty0 + wy + R;
-        const T* rowz = sz + hy * HW + tx + R;
-        const WT* rowg = sg + hy * HW + tx + R;
-        WT row[K3_RB];
-#pragma unroll
-        for (int r = 0; r < K3_RB; ++r) row[r] = WT(0);
-        if ((wy >= K3_RB - 1 - R) && (wy <= R)) {
-            // this window row reaches every owned pixel: straight-line RB pairs
-            if (interior_x) {
-#pragma unroll 2
-                for (int wx = -R; wx <= R; ++wx) {
-                    T zj[9];
-                    POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
-                    const WT gj = rowg[wx];
-#pragma unroll
-                    for (int r = 0; r < K3_RB; ++r) row[r] += pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
-                }
-            } else {
-                for (int wx = -R; wx <= R; ++wx) {
-                    T zj[9];
-                    POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
-                    const WT gj = rowg[wx];
-                    const bool colok = gx + wx >= 0 && gx + wx < width;
-#pragma unroll
-                    for (int r = 0; r < K3_RB; ++r) {
-                        WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
-                        row[r] += colok ? w : WT(0);
-                    }
-                }
-            }
-        } else {
-            // one of the RB-1 rows at either end: only some owned pixels reach it
-            for (int wx = -R; wx <= R; ++wx) {
-                T zj[9];
-                POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-#pragma unroll
-                for (int k = 0; k < 9; ++k) zj[k] = rowz[k * HP + wx];
-                const WT gj = rowg[wx];
-                const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-#pragma unroll
-                for (int r = 0; r < K3_RB; ++r) {
-                    const int dy = wy - r;
-                    if (dy >= -R && dy <= R) {  // warp-uniform
-                        WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
-                        row[r] += colok ? w : WT(0);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < K3_RB; ++r) acc[r] += (double)row[r];
-    }
-#pragma unroll
-    for (int r = 0; r < K3_RB; ++r) {
-        const int64_t gy = y0 + ty0 + r;
-        if (gx < width && gy < row_end) out[(gy - row_begin) * width + gx] = (S)acc[r];
-    }
-}
-
-template <typename S, typename T, typename WT, int TY>
-int launch_window_ty(const S* z, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                     int64_t re, int R, double alpha, const WT* g, S* out, size_t smem,
-                     cudaStream_t s) {
-    constexpr int K3_RB = K3_RB_FOR<TY>::v;
-    auto kern = k_window_sum<S, T, WT, TY, K3_RB>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
-    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - rb + TY - 1) / TY));
-    kern<<<grid, K3_TX * TY / K3_RB, smem, s>>>(z, ld, width, slab_rows, rb, re, R, g, alpha,
-                                                alpha == 2.0 ? 1 : 0, out);
-    return launch_check("polsar_window_distance: launch failed");
-}
-
-constexpr size_t K3_SMEM_MAX = 227 * 1024;
-
-template <typename T, typename WT>
-size_t window_smem(int TY, int R) {
-    return (size_t)(K3_TX + 2 * R) * (TY + 2 * R) * (9 * sizeof(T) + sizeof(WT));
-}
-
-template <typename S, typename T, typename WT>
-int launch_window(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                  int64_t re, int R, double looks, double h, void* ws, void* outv,
-                  cudaStream_t s) {
-    const S* z = (const S*)zv;
-    WT* g = (WT*)ws;
-    int64_t n = slab_rows * width;
-    k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
-    const double alpha = looks / (2.0 * h);
-    S* out = (S*)outv;
-    if (window_smem<T, WT>(32, R) <= K3_SMEM_MAX)
-        return launch_window_ty<S, T, WT, 32>(z, ld, width, slab_rows, rb, re, R, alpha, g, out,
-                                              window_smem<T, WT>(32, R), s);
-    if (window_smem<T, WT>(16, R) <= K3_SMEM_MAX)
-        return launch_window_ty<S, T, WT, 16>(z, ld, width, slab_rows, rb, re, R, alpha, g, out,
-                                              window_smem<T, WT>(16, R), s);
-    if (window_smem<T, WT>(8, R) <= K3_SMEM_MAX)
-        return launch_window_ty<S, T, WT, 8>(z, ld, width, slab_rows, rb, re, R, alpha, g, out,
-                                             window_smem<T, WT>(8, R), s);
-    return fail(POLSAR_ENOTSUP, "polsar_window_distance: radius too large for shared memory");
-}
-
-// ------------------------------------------------------------------------
-// K4: non-local-means filter output (the NLM filter with
-// stochastic distances of PAPER.md:77-80 [§I]).  Same pair weights as K3 and
-// in the same pass, accumulated with the window pixels themselves:
-//   W_i = sum_j w_ij,   Zhat_i = sum_j w_ij Z_j / W_i   (9 packed planes).
-// Layout and staging as k_window_sum; the weighted sums accumulate in the
-// pair-determinant type (fp64 for the default modes: one F2F, one DADD and
-// nine DFMA per pair on top of the determinant).
-template <typename S, typename T, typename WT, int TY, int RB>
-__global__ void __launch_bounds__(K3_TX * TY / RB, 1)
-k_nlm_sum(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
-          int64_t row_begin, int64_t row_end, int R, const WT* __restrict__ g, double alpha_d,
-          int alpha_is_2, S* __restrict__ out_w, S* __restrict__ out_z, int64_t ld_out) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int HW = K3_TX + 2 * R;
-    const int HH = TY + 2 * R;
-    const int HP = HW * HH;
-    T* sz = reinterpret_cast<T*>(smem_raw);  // HP records of 10 T (load_rec)
-
-    const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
-    const int64_t y0 = row_begin + (int64_t)blockIdx.y * TY;
-    for (int q = threadIdx.x; q < HP; q += blockDim.x) {
-        int hy = q / HW, hx = q % HW;
-        int64_t gy = y0 - R + hy, gx = x0 - R + hx;
-        bool in = gy >= 0 && gy < slab_rows && gx >= 0 && gx < width;
-        int64_t p = in ? gy * width + gx : 0;
-        T* rec = sz + 10 * q;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) rec[k] = in ? (T)z[k * ld + p] : T(0);
-        rec[9] = pack_g<T, WT>(in ? g[p] : WT(0));
-    }
-    __syncthreads();
-
-    const int tx = threadIdx.x % K3_TX;
-    const int ty0 = (threadIdx.x / K3_TX) * RB;
-    const int64_t gx = x0 + tx;
-    T zi[RB][9], accz[RB][9], accw[RB];
-    WT gi[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        load_rec(sz + 10 * ((ty0 + r + R) * HW + (tx + R)), zi[r], gi[r]);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) accz[r][k] = T(0);
-        accw[r] = T(0);
-    }
-    const WT alpha = (WT)alpha_d;
-    const bool a2 = alpha_is_2 != 0;
-    const bool interior_x = (x0 - R >= 0) && (x0 + K3_TX + R <= width);
-
-    for (int wy = -R; wy <= R + RB - 1; ++wy) {
-        const int64_t gyj = y0 + ty0 + wy;
-        if (gyj < 0 || gyj >= slab_rows) continue;  // warp-uniform
-        const int hy = ty0 + wy + R;
-        const T* rec = sz + 10 * (hy * HW + tx);  // neighbour wx = -R
-        bool rok[RB];
-#pragma unroll
-        for (int r = 0; r < RB; ++r) rok[r] = (wy - r >= -R) && (wy - r <= R);  // warp-uniform
-        for (int wx = -R; wx <= R; ++wx, rec += 10) {
-            T zj[9];
-            WT gj;
-            POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-            load_rec(rec, zj, gj);
-            const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-#pragma unroll
-            for (int r = 0; r < RB; ++r) {
-                if (rok[r]) {
-                    WT w = pair_w<T, WT>(zi[r], gi[r], zj, gj, alpha, a2);
-                    const T wt = colok ? (T)w : T(0);
-                    accw[r] = ADD(accw[r], wt);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) accz[r][k] = FMA(wt, zj[k], accz[r][k]);
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        const int64_t gy = y0 + ty0 + r;
-        if (gx < width && gy < row_end) {
-            const int64_t o = (gy - row_begin) * width + gx;
-            if (out_w) out_w[o] = (S)accw[r];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) out_z[k * ld_out + o] = (S)(accz[r][k] / accw[r]);
-        }
-    }
-}
-
-template <typename S, typename T, typename WT>
-int launch_nlm(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re,
-               int R, double looks, double h, void* ws, void* out_w, void* out_z, int64_t ld_out,
-               cudaStream_t s) {
-    const S* z = (const S*)zv;
-    WT* g = (WT*)ws;
-    const int64_t n = slab_rows * width;
-    k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
-    const double alpha = looks / (2.0 * h);
-    auto nlm_smem = [R](int ty) { return (size_t)(K3_TX + 2 * R) * (ty + 2 * R) * 10 * sizeof(T); };
-    int TY = 16;
-    size_t smem = nlm_smem(16);
-    if (smem > K3_SMEM_MAX) {
-        TY = 8;
-        smem = nlm_smem(8);
-        if (smem > K3_SMEM_MAX)
-            return fail(POLSAR_ENOTSUP, "polsar_nlm_filter: radius too large for shared memory");
-    }
-    auto kern = TY == 16 ? k_nlm_sum<S, T, WT, 16, 2> : k_nlm_sum<S, T, WT, 8, 2>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_nlm_filter: shared memory request too large");
-    dim3 grid((unsigned)((width + K3_TX - 1) / K3_TX), (unsigned)((re - rb + TY - 1) / TY));
-    kern<<<grid, K3_TX * TY / 2, smem, s>>>(z, ld, width, slab_rows, rb, re, R, g, alpha,
-                                            alpha == 2.0 ? 1 : 0, (S*)out_w, (S*)out_z, ld_out);
-    return launch_check("polsar_nlm_filter: launch failed");
-}
-
-// ------------------------------------------------------------------------
-// K3 (v3, the fp64-determinant modes): the pair determinant by the 3x3
-// expansion  det(A + B) = det A + det B + <adj A, B> + <A, adj B>,
-// <X, Y> = tr(X Y) = sum_k w_k x_k y_k over the packed components with
-// w = (1, 2, 2, 2, 2, 1, 2, 2, 1).  Alg. 2's cofactors (Eq. 3) and
-// determinant (Eq. 6) are evaluated ONCE per pixel in the prepass; each pair
-// then costs one add and 18 FMAs instead of 9 adds and 20 multiply-adds
-// (S = Z_i + Z_j, then Eq. 6 on S).  All four terms are >= 0 for positive-
-// definite pixels, so the sum itself cannot cancel.
-//
-// Prepass (K3a v3) writes 20 fp64 planes per slab pixel:
-//   0..8   z   (the packed Z)
-//   9..17  u = w * adj(Z) (cofactors a_c, b_c, c_c, d_c, e_c, f_c, weighted)
-//   18     D = det Z (Eq. 6)
-//   19     g = 1 / (8 D) as float in the low 4 bytes
-// Main pass (K3b v3): a CTA owns a 256-column x RB-row output block (each
-// thread one column, RB rows).  The window rows it needs stream through
-// shared memory V3_CH rows at a time (all 20 planes, 256 + 2R' columns),
-// double-buffered with cp.async so the next rows load while the current ones
-// are consumed.  Every thread of the CTA pairs each staged row with the same
-// owned rows, so the per-row work is identical across warps (no barrier
-// imbalance), and each staged Z_j serves RB pairs.
-constexpr int V3_TX = 256;
-constexpr int V3_RB = 4;
-constexpr int V3_CH = 2;
-constexpr int V3_NP = 20;        // planes per pixel
-constexpr int V3_THREADS = V3_TX;
-constexpr int V3_RMAX = 12;      // radius limit of this kernel (the paper's R = 11)
-constexpr int V3_XOFF = V3_RMAX; // column of x0 inside a staged row (even)
-constexpr int V3_SW = V3_TX + 2 * V3_XOFF;  // staged row width (compile-time strides)
-constexpr int V3_CHP = V3_CH * V3_SW;       // pixels per chunk plane
-
-// KL prepass: planes 9..17 hold w * Z^-1 from Alg. 2
-// (K1's device function: cofactors, Eq. 6 det, t = 1/det, scale), plane 18
-// holds 0, so the pair sum T = <X_i, Z_j> + <Z_i, X_j> = tr(Z_i^-1 Z_j) +
-// tr(Z_j^-1 Z_i).
-template <typename S>
-__global__ void __launch_bounds__(256)
-k_window_prep_kl(const S* __restrict__ z, int64_t ld, int64_t n, double* __restrict__ ws) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        H9<double> m;
-        m.a = (double)z[0 * ld + p];
-        m.br = (double)z[1 * ld + p];
-        m.bi = (double)z[2 * ld + p];
-        m.cr = (double)z[3 * ld + p];
-        m.ci = (double)z[4 * ld + p];
-        m.d = (double)z[5 * ld + p];
-        m.er = (double)z[6 * ld + p];
-        m.ei = (double)z[7 * ld + p];
-        m.f = (double)z[8 * ld + p];
-        double x[9], det, t;
-        alg2_plain<double>(m, x, det, t);
-        const int64_t P = n;
-        ws[0 * P + p] = m.a;  ws[1 * P + p] = m.br; ws[2 * P + p] = m.bi;
-        ws[3 * P + p] = m.cr; ws[4 * P + p] = m.ci; ws[5 * P + p] = m.d;
-        ws[6 * P + p] = m.er; ws[7 * P + p] = m.ei; ws[8 * P + p] = m.f;
-        const double wk[9] = {1, 2, 2, 2, 2, 1, 2, 2, 1};
-        // X = NaN marks a pixel that is not positive definite (as g in k_window_prep)
-        const bool ok = det > 0.0 && t < INFINITY;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) ws[(9 + k) * P + p] = ok ? wk[k] * x[k] : NAN;
-        ws[18 * P + p] = 0.0;
-        ws[19 * P + p] = 0.0;
-    }
-}
-
-template <typename S, typename WT>
-__global__ void __launch_bounds__(256)
-k_window_prep_v3(const S* __restrict__ z, int64_t ld, int64_t n, double* __restrict__ ws) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        H9<double> m;
-        m.a = (double)z[0 * ld + p];
-        m.br = (double)z[1 * ld + p];
-        m.bi = (double)z[2 * ld + p];
-        m.cr = (double)z[3 * ld + p];
-        m.ci = (double)z[4 * ld + p];
-        m.d = (double)z[5 * ld + p];
-        m.er = (double)z[6 * ld + p];
-        m.ei = (double)z[7 * ld + p];
-        m.f = (double)z[8 * ld + p];
-        // Eq. 3 cofactors (Alg. 2 step 1) and Eq. 6 determinant (step 2)
-        double ac = FMA(m.d, m.f, -FMA(m.er, m.er, MUL(m.ei, m.ei)));
-        double bcr = FMA(m.cr, m.er, FMA(m.ci, m.ei, -MUL(m.br, m.f)));
-        double bci = FMA(m.ci, m.er, -FMA(m.cr, m.ei, MUL(m.bi, m.f)));
-        double ccr = FMA(m.br, m.er, -FMA(m.bi, m.ei, MUL(m.cr, m.d)));
-        double cci = FMA(m.br, m.ei, FMA(m.bi, m.er, -MUL(m.ci, m.d)));
-        double dc = FMA(m.a, m.f, -FMA(m.cr, m.cr, MUL(m.ci, m.ci)));
-        double ecr = FMA(m.cr, m.br, FMA(m.ci, m.bi, -MUL(m.a, m.er)));
-        double eci = FMA(m.ci, m.br, -FMA(m.cr, m.bi, MUL(m.a, m.ei)));
-        double fc = FMA(m.a, m.d, -FMA(m.br, m.br, MUL(m.bi, m.bi)));
-        double det = FMA(m.a, ac, FMA(m.br, bcr, FMA(m.bi, bci, FMA(m.cr, ccr, MUL(m.ci, cci)))));
-        const int64_t P = n;  // plane stride of the workspace
-        ws[0 * P + p] = m.a;  ws[1 * P + p] = m.br; ws[2 * P + p] = m.bi;
-        ws[3 * P + p] = m.cr; ws[4 * P + p] = m.ci; ws[5 * P + p] = m.d;
-        ws[6 * P + p] = m.er; ws[7 * P + p] = m.ei; ws[8 * P + p] = m.f;
-        ws[9 * P + p] = ac;
-        ws[10 * P + p] = 2.0 * bcr; ws[11 * P + p] = 2.0 * bci;
-        ws[12 * P + p] = 2.0 * ccr; ws[13 * P + p] = 2.0 * cci;
-        ws[14 * P + p] = dc;
-        ws[15 * P + p] = 2.0 * ecr; ws[16 * P + p] = 2.0 * eci;
-        ws[17 * P + p] = fc;
-        ws[18 * P + p] = det;
-        const double g = 1.0 / (8.0 * det);
-        if constexpr (std::is_same<WT, float>::value)
-            ws[19 * P + p] = __longlong_as_double((long long)(unsigned)__float_as_uint((float)g));
-        else
-            ws[19 * P + p] = g;
-    }
-}
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    int src_bytes = valid ? 8 : 0;  // 0: zero-fill
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(sa), "l"(gmem), "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
-
-// plane 19 holds g as fp64 (fp64 weights) or as fp32 bits in the low word
-template <typename WT>
-__device__ __forceinline__ WT load_g(double v);
-template <>
-__device__ __forceinline__ float load_g<float>(double v) {
-    return __uint_as_float((unsigned)__double_as_longlong(v));
-}
-template <>
-__device__ __forceinline__ double load_g<double>(double v) { return v; }
-
-// Weight of a pair for the symmetric Wishart KL distance:
-// T = tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i), d = L (T/2 - 3), w = exp(-d/h);
-// lk = L/h.  The subtraction is done in fp64 (T/2 ~ 3 for similar pixels).
-template <typename WT>
-__device__ __forceinline__ WT weight_kl(double T, WT lk);
-template <>
-__device__ __forceinline__ float weight_kl<float>(double T, float lk) {
-    const float d = (float)__fma_rn(T, 0.5, -3.0);
-    return fast_exp2(-lk * d * 1.4426950408889634f);
-}
-template <>
-__device__ __forceinline__ double weight_kl<double>(double T, double lk) {
-    return exp(-lk * __fma_rn(T, 0.5, -3.0));
-}
-
-template <typename WT>
-__device__ __forceinline__ WT weight_v3(double T, WT gi, WT gj, WT alpha, bool a2) {
-    WT ft = (WT)T;
-    WT rr = (ft * gi) * (ft * gj);
-    return pair_weight(rr, alpha, a2);
-}
-
-// one pair: T = det(Z_i + Z_j) = D_i + D_j + <u_i, z_j> + <z_i, u_j>
-__device__ __forceinline__ double pair_T(const double* ui, const double* zi, double Di,
-                                         const double* uj, const double* zj, double Dj) {
-    double a = __fma_rn(ui[0], zj[0], __dadd_rn(Di, Dj));
-    double b = __dmul_rn(ui[6], zj[6]);
-    double c = __dmul_rn(zi[3], uj[3]);
-    a = __fma_rn(ui[1], zj[1], a);
-    b = __fma_rn(ui[7], zj[7], b);
-    c = __fma_rn(zi[4], uj[4], c);
-    a = __fma_rn(ui[2], zj[2], a);
-    b = __fma_rn(ui[8], zj[8], b);
-    c = __fma_rn(zi[5], uj[5], c);
-    a = __fma_rn(ui[3], zj[3], a);
-    b = __fma_rn(zi[0], uj[0], b);
-    c = __fma_rn(zi[6], uj[6], c);
-    a = __fma_rn(ui[4], zj[4], a);
-    b = __fma_rn(zi[1], uj[1], b);
-    c = __fma_rn(zi[7], uj[7], c);
-    a = __fma_rn(ui[5], zj[5], a);
-    b = __fma_rn(zi[2], uj[2], b);
-    c = __fma_rn(zi[8], uj[8], c);
-    return __dadd_rn(a, __dadd_rn(b, c));
-}
-
-
-// T_r = det(Z_{i_r} + Z_j) for the RB owned pixels at once, written as
-// 2*RB independent FMA chains (k-outer, pixel-inner) so the FP64 pipe always
-// has independent work in flight.
-template <int RB>
-__device__ __forceinline__ void pair_T_block(const double (&ui)[RB][9], const double (&zi)[RB][9],
-                                             const double (&Di)[RB], const double* uj,
-                                             const double* zj, double Dj, double (&T)[RB]) {
-    double A[RB], B[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        A[r] = __fma_rn(ui[r][0], zj[0], Di[r]);
-        B[r] = __fma_rn(zi[r][0], uj[0], Dj);
-    }
-#pragma unroll
-    for (int k = 1; k < 9; ++k) {
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            A[r] = __fma_rn(ui[r][k], zj[k], A[r]);
-            B[r] = __fma_rn(zi[r][k], uj[k], B[r]);
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r) T[r] = __dadd_rn(A[r], B[r]);
-}
-
-enum { DIST_LOGDET = 0, DIST_KL = 1 };
-
-template <int KIND, typename WT>
-__device__ __forceinline__ WT weight_kind(double T, WT gi, WT gj, WT alpha, bool a2) {
-    if constexpr (KIND == DIST_KL)
-        return weight_kl<WT>(T, alpha);
-    else
-        return weight_v3<WT>(T, gi, gj, alpha, a2);
-}
-
-template <typename S, typename WT, bool A2, int KIND = DIST_LOGDET>
-__global__ void __launch_bounds__(V3_THREADS, 1)
-k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows, int64_t row_begin,
-                int64_t row_end, int R, double alpha_d, S* __restrict__ out) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int XOFF = V3_XOFF, SW = V3_SW, CHP = V3_CHP;
-    double* buf = reinterpret_cast<double*>(smem_raw);  // [2][V3_NP][V3_CH][SW]
-    const int64_t P = slab_rows * width;                // workspace plane stride
-
-    const int64_t x0 = (int64_t)blockIdx.x * V3_TX;
-    const int64_t y0 = row_begin + (int64_t)blockIdx.y * V3_RB;
-    // window rows of the block, clipped to the slab
-    const int64_t ja = y0 - R > 0 ? y0 - R : 0;
-    const int64_t jb = (y0 + V3_RB - 1 + R) < slab_rows - 1 ? (y0 + V3_RB - 1 + R) : slab_rows - 1;
-    const int nrows = (int)(jb - ja + 1);
-    const int nchunks = (nrows + V3_CH - 1) / V3_CH;
-
-    auto load_chunk = [&](int c, int b) {
-        double* dst = buf + (size_t)b * V3_NP * CHP;
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        for (int pr = warp; pr < V3_NP * V3_CH; pr += V3_THREADS / 32) {
-            const int pl = pr / V3_CH, row = pr % V3_CH;  // compile-time divisors
-            const int64_t gy = ja + (int64_t)c * V3_CH + row;
-            const bool rok = gy <= jb;
-            const double* srow = ws + pl * P + (rok ? gy : 0) * width;
-            double* drow = dst + pl * CHP + row * SW;
-            for (int col = lane; col < SW; col += 32) {
-                POLSAR_CHECK(pl * CHP + row * SW + col < V3_NP * CHP);
-                const int64_t gxx = x0 - XOFF + col;
-                const bool ok = rok && gxx >= 0 && gxx < width;
-                cp_async8(drow + col, srow + (ok ? gxx : 0), ok);
-            }
-        }
-        cp_async_commit();
-    };
-    load_chunk(0, 0);
-
-    // owned pixels: column gx, rows y0 .. y0 + RB - 1
-    const int tx = threadIdx.x;
-    const int64_t gx = x0 + tx;
-    double ui[V3_RB][9], zi[V3_RB][9], Di[V3_RB];
-    WT gi[V3_RB];
-    double acc[V3_RB];
-#pragma unroll
-    for (int r = 0; r < V3_RB; ++r) {
-        const int64_t gy = y0 + r;
-        const bool ok = gx < width && gy < slab_rows;
-        const int64_t p = ok ? gy * width + gx : 0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            zi[r][k] = ok ? ws[k * P + p] : 0.0;
-            ui[r][k] = ok ? ws[(9 + k) * P + p] : 0.0;
-        }
-        Di[r] = ok ? ws[18 * P + p] : 0.0;
-        gi[r] = ok ? load_g<WT>(ws[19 * P + p]) : WT(0);
-        acc[r] = 0.0;
-    }
-    const WT alpha = (WT)alpha_d;
-    constexpr bool a2 = A2;
-    const bool interior_x = (x0 - R >= 0) && (x0 + V3_TX + R <= width);
-
-    for (int c = 0; c < nchunks; ++c) {
-        if (c + 1 < nchunks) {
-            load_chunk(c + 1, (c + 1) & 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const double* cb = buf + (size_t)(c & 1) * V3_NP * CHP;
-#pragma unroll 1
-        for (int row = 0; row < V3_CH; ++row) {
-            const int64_t gyj = ja + (int64_t)c * V3_CH + row;
-            if (gyj > jb) break;
-            const int dy0 = (int)(gyj - y0);  // dy of owned row r is dy0 - r (CTA-uniform)
-            const double* rb = cb + row * SW + XOFF + tx;
-            WT rowacc[V3_RB];
-#pragma unroll
-            for (int r = 0; r < V3_RB; ++r) rowacc[r] = WT(0);
-            const bool all = (dy0 - (V3_RB - 1) >= -R) && (dy0 <= R);
-            if (all) {
-                // software-pipelined: the weights of column wx-1 (F2F / FMUL /
-                // MUFU, long-latency) are evaluated alongside the FMA chains of
-                // column wx, so the FP64 pipe never waits on the weight tail
-                double Tp[V3_RB];
-                WT gp = WT(0);
-                bool okp = false;
-#pragma unroll
-                for (int r = 0; r < V3_RB; ++r) Tp[r] = 1.0;
-#pragma unroll 1
-                for (int wx = -R; wx <= R; ++wx) {
-                    double zj[9], uj[9];
-                    POLSAR_CHECK(row * SW + XOFF + tx + wx >= 0 && row * SW + XOFF + tx + wx < CHP);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) {
-                        zj[k] = rb[k * CHP + wx];
-                        uj[k] = rb[(9 + k) * CHP + wx];
-                    }
-                    const double Dj = rb[18 * CHP + wx];
-                    const WT gj = load_g<WT>(rb[19 * CHP + wx]);
-                    const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-                    double T[V3_RB];
-                    pair_T_block<V3_RB>(ui, zi, Di, uj, zj, Dj, T);
-#pragma unroll
-                    for (int r = 0; r < V3_RB; ++r) {
-                        WT w = weight_kind<KIND, WT>(Tp[r], gi[r], gp, alpha, a2);
-                        rowacc[r] += okp ? w : WT(0);
-                        Tp[r] = T[r];
-                    }
-                    gp = gj;
-                    okp = colok;
-                }
-#pragma unroll
-                for (int r = 0; r < V3_RB; ++r) {
-                    WT w = weight_kind<KIND, WT>(Tp[r], gi[r], gp, alpha, a2);
-                    rowacc[r] += okp ? w : WT(0);
-                }
-            } else {
-#pragma unroll 1
-                for (int wx = -R; wx <= R; ++wx) {
-                    double zj[9], uj[9];
-                    POLSAR_CHECK(row * SW + XOFF + tx + wx >= 0 && row * SW + XOFF + tx + wx < CHP);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) {
-                        zj[k] = rb[k * CHP + wx];
-                        uj[k] = rb[(9 + k) * CHP + wx];
-                    }
-                    const double Dj = rb[18 * CHP + wx];
-                    const WT gj = load_g<WT>(rb[19 * CHP + wx]);
-                    const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-#pragma unroll
-                    for (int r = 0; r < V3_RB; ++r) {
-                        const int dy = dy0 - r;
-                        if (dy >= -R && dy <= R) {  // CTA-uniform
-                            WT w = weight_kind<KIND, WT>(pair_T(ui[r], zi[r], Di[r], uj, zj, Dj), gi[r], gj, alpha, a2);
-                            rowacc[r] += colok ? w : WT(0);
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < V3_RB; ++r) acc[r] += (double)rowacc[r];
-        }
-        __syncthreads();  // buffer (c & 1) is refilled by the prefetch of chunk c + 2
-    }
-#pragma unroll
-    for (int r = 0; r < V3_RB; ++r) {
-        const int64_t gy = y0 + r;
-        if (gx < width && gy < row_end) out[(gy - row_begin) * width + gx] = (S)acc[r];
-    }
-}
-
-template <typename S, typename WT>
-int launch_window_v3(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                     int64_t re, int R, double looks, double h, void* wsv, void* outv,
-                     cudaStream_t s) {
-    const int64_t n = slab_rows * width;
-    double* ws = (double*)wsv;
-    k_window_prep_v3<S, WT><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, ws);
-    size_t smem = (size_t)2 * V3_NP * V3_CHP * sizeof(double);
-    const double alpha = looks / (2.0 * h);
-    auto kern = alpha == 2.0 ? k_window_sum_v3<S, WT, true> : k_window_sum_v3<S, WT, false>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
-    dim3 grid((unsigned)((width + V3_TX - 1) / V3_TX), (unsigned)((re - rb + V3_RB - 1) / V3_RB));
-    kern<<<grid, V3_THREADS, smem, s>>>(ws, width, slab_rows, rb, re, R, alpha, (S*)outv);
-    return launch_check("polsar_window_distance: launch failed");
-}
-
-template <typename S, typename WT>
-int launch_window_kl(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                     int64_t re, int R, double looks, double h, void* wsv, void* outv,
-                     cudaStream_t s) {
-    const int64_t n = slab_rows * width;
-    double* ws = (double*)wsv;
-    k_window_prep_kl<S><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, ws);
-    size_t smem = (size_t)2 * V3_NP * V3_CHP * sizeof(double);
-    auto kern = k_window_sum_v3<S, WT, false, DIST_KL>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_window_kl: shared memory request too large");
-    dim3 grid((unsigned)((width + V3_TX - 1) / V3_TX), (unsigned)((re - rb + V3_RB - 1) / V3_RB));
-    kern<<<grid, V3_THREADS, smem, s>>>(ws, width, slab_rows, rb, re, R, looks / h, (S*)outv);
-    return launch_check("polsar_window_kl: launch failed");
-}
-
-// Window kernel variant (R <= 12): 4 (symmetric two-pass, default), 2 (direct
-// Eq. 6 on S = Z_i + Z_j for every ordered pair), 3 (cubic expansion over
-// per-pixel adjugates).  POLSAR_WINDOW_VARIANT=2|3 selects the alternatives
-// for A/B runs; all are parity-tested.  R > 12 always runs variant 2.
-// (read once; function-local static initialisation is thread-safe)
-int window_variant() {
-    static const int v = [] {
-        const char* e = getenv("POLSAR_WINDOW_VARIANT");
-        return (e && (e[0] == '2' || e[0] == '3')) ? e[0] - '0' : 4;
-    }();
-    return v;
-}
-
-// ------------------------------------------------------------------------
-// K3 (symmetric, default for R <= V3_RMAX): d_ij = d_ji (the window is
-// symmetric and det((Z_i+Z_j)/2) is), so each unordered pair is evaluated
-// once.  Pass 1 (k_window_fwd) computes, for every pixel i, the weights of its
-// 2R(R+1) "forward" neighbours j = i + delta (delta_y > 0, or delta_y = 0 and
-// delta_x > 0) and their sum F_i.  Each weight must also reach W_j:
-//  * ACC form (default for the window and KL): added to j's backward sum in
-//    shared memory as an exact fixed-point integer (acc_add below); pass 2
-//    (k_window_bwd_acc) adds the <= 4 tile sums of each pixel.
-//  * plane form (NLM, whose gather reads the weights; POLSAR_WINDOW_PLANES=1):
-//    stored at wbuf[delta][i]; pass 2 (k_window_bwd) adds, for every output
-//    pixel j, W_j = 1 + F_j + sum_delta wbuf[delta][j - delta] (1068 B/pixel
-//    of workspace traffic at R = 11, fp32 weights).
-// d_jj = 0 contributes exactly 1.  Half the FP64 work of k_window_sum; every
-// sum is exact or in a fixed order, so results are bit-reproducible and slab
-// decompositions are exact.
-__host__ __device__ __forceinline__ int fwd_count(int R) { return 2 * R * (R + 1); }
-// Row pitch of the weight planes: width rounded up to 16 bytes, so every row
-// of every plane starts 16-byte aligned (the TMA tiles of the NLM gather need
-// 16-byte aligned starts: measured, tools/micro/tma1d_test.cu).
-template <typename WT>
-__host__ __device__ __forceinline__ int64_t weight_pitch(int64_t width) {
-    constexpr int64_t a = 16 / sizeof(WT);
-    return (width + a - 1) / a * a;
-}
-__device__ __forceinline__ int fwd_index(int dy, int dx, int R) {
-    return dy == 0 ? dx - 1 : R + (dy - 1) * (2 * R + 1) + (dx + R);
-}
-
-#ifndef POLSAR_SYM_TY
-#define POLSAR_SYM_TY 32
-#endif
-#ifndef POLSAR_SYM_RB
-#define POLSAR_SYM_RB 2
-#endif
-#ifndef POLSAR_SYM_UNROLL
-#define POLSAR_SYM_UNROLL 2
-#endif
-constexpr int kSymUnroll = POLSAR_SYM_UNROLL;
-
-// Pair policies of pass 1: what a shared-memory record holds (RS slots of T)
-// and how a pair weight is computed from two records.
-//
-// Log-det distance (R-12): 9 planes + g = 1/(8 det Z); w from Eq. 6 on
-// S = Z_i + Z_j (pair_w).
-template <typename S_, typename T_, typename WT_, int A2_ = -1>
-struct LogDetPair {
-    // A2_: 1 / 0 fix "alpha == 2" at compile time (the weight is 1/r^2, or
-    // MUFU lg2/ex2); -1 reads the runtime flag a2
-    using S = S_;
-    using T = T_;
-    using WT = WT_;
-    static constexpr int RS = 10;
-    struct Rec {
-        T z[9];
-        WT g;
-    };
-    const S* z;
-    int64_t ld;
-    const WT* g;
-    WT alpha;
-    bool a2;
-    __device__ __forceinline__ void fill(T* rec, int64_t p, bool in) const {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) rec[k] = in ? (T)z[k * ld + p] : T(0);
-        rec[9] = pack_g<T, WT>(in ? g[p] : WT(0));
-    }
-    __device__ __forceinline__ static void load(const T* rec, Rec& r) { load_rec(rec, r.z, r.g); }
-    // (k_window_prep's NaN mark)
-    __device__ __forceinline__ static bool invalid(const Rec& r) { return !(r.g > WT(0)); }
-    // weight = post(pre(i, j), i, aux(j)): pre is the FP64 part (det of
-    // S = Z_i + Z_j by Eq. 6), post the fp32 weight (same arithmetic as pair_w)
-#ifndef POLSAR_LOGDET_PIPELINE
-#define POLSAR_LOGDET_PIPELINE 0
-#endif
-    static constexpr bool kPipeline = POLSAR_LOGDET_PIPELINE;  // measured: pipelining costs 4 % here
-    using Q = T;
-    using Aux = WT;
-    __device__ __forceinline__ Q pre(const Rec& i, const Rec& j) const {
-        return det_eq6<T>(ADD(i.z[0], j.z[0]), ADD(i.z[1], j.z[1]), ADD(i.z[2], j.z[2]),
-                          ADD(i.z[3], j.z[3]), ADD(i.z[4], j.z[4]), ADD(i.z[5], j.z[5]),
-                          ADD(i.z[6], j.z[6]), ADD(i.z[7], j.z[7]), ADD(i.z[8], j.z[8]));
-    }
-    __device__ __forceinline__ static Aux aux(const Rec& j) { return j.g; }
-    __device__ __forceinline__ WT post(Q ds, const Rec& i, Aux gj) const {
-        WT fds = (WT)ds;
-        WT rr = (fds * i.g) * (fds * gj);
-        return pair_weight(rr, alpha, A2_ < 0 ? a2 : A2_ == 1);
-    }
-    __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
-        return post(pre(i, j), i, aux(j));
-    }
-};
-
-// Symmetric Wishart KL (K6): Z and X = w * Z^-1 (Alg. 2 in k_window_prep_kl,
-// w the Hermitian trace weights), T = <X_i, Z_j> + <Z_i, X_j>
-// = tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i), w = exp(-L (T/2 - 3) / h).
-template <typename WT_>
-struct KLPair {
-    using T = double;
-    using WT = WT_;
-    static constexpr int RS = 18;
-    struct Rec {
-        double z[9];
-        double x[9];
-    };
-    const double* ws;  // prep planes 0..8 = Z, 9..17 = X, plane stride P
-    int64_t P;
-    WT lk;             // L / h
-    __device__ __forceinline__ void fill(double* rec, int64_t p, bool in) const {
-#pragma unroll
-        for (int k = 0; k < 18; ++k) rec[k] = in ? ws[k * P + p] : 0.0;
-    }
-    __device__ __forceinline__ static void load(const double* rec, Rec& r) {
-        const double2* v = reinterpret_cast<const double2*>(rec);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            const double2 u = v[k];
-            const int a = 2 * k, b = 2 * k + 1;
-            (a < 9 ? r.z[a] : r.x[a - 9]) = u.x;
-            (b < 9 ? r.z[b] : r.x[b - 9]) = u.y;
-        }
-    }
-    static constexpr bool kPipeline = true;  // measured: 4.79 -> 4.43 ms on c5
-    __device__ __forceinline__ static bool invalid(const Rec& r) { return r.x[0] != r.x[0]; }  // NaN mark
-    using Q = double;
-    using Aux = int;
-    __device__ __forceinline__ Q pre(const Rec& i, const Rec& j) const {
-        double A = __dmul_rn(i.x[0], j.z[0]);
-        double B = __dmul_rn(i.z[0], j.x[0]);
-#pragma unroll
-        for (int k = 1; k < 9; ++k) {
-            A = __fma_rn(i.x[k], j.z[k], A);
-            B = __fma_rn(i.z[k], j.x[k], B);
-        }
-        return __dadd_rn(A, B);
-    }
-    __device__ __forceinline__ static Aux aux(const Rec&) { return 0; }
-    __device__ __forceinline__ WT post(Q T, const Rec&, Aux) const { return weight_kl<WT>(T, lk); }
-    __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
-        return post(pre(i, j), i, aux(j));
-    }
-};
-
-// KL with fp32 storage: Z is exact in fp32, so the record keeps X (9 fp64)
-// and Z (9 fp32, widened on load): 112 bytes instead of 144 (KL's pass 1 is
-// bound by shared-memory bandwidth).  Same arithmetic as KLPair.
-template <typename WT_>
-struct KLPairF {
-    using T = double;
-    using WT = WT_;
-    static constexpr int RS = 14;  // 112 bytes: X0..X8 (fp64), Z0..Z8 (fp32) at byte 72, pad
-    using Rec = typename KLPair<WT_>::Rec;
-    const double* ws;  // prep planes 0..8 = Z, 9..17 = X, plane stride P
-    int64_t P;
-    WT lk;             // L / h
-    __device__ __forceinline__ void fill(double* rec, int64_t p, bool in) const {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) rec[k] = in ? ws[(9 + k) * P + p] : 0.0;
-        float* zf = reinterpret_cast<float*>(rec + 9);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) zf[k] = in ? (float)ws[k * P + p] : 0.0f;  // exact: Z came from fp32
-        zf[9] = 0.0f;
-    }
-    __device__ __forceinline__ static void load(const double* rec, Rec& r) {
-        const double2* v = reinterpret_cast<const double2*>(rec);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const double2 u = v[k];
-            r.x[2 * k] = u.x;
-            r.x[2 * k + 1] = u.y;
-        }
-        r.x[8] = rec[8];
-        const float2 a = *reinterpret_cast<const float2*>(rec + 9);          // byte 72
-        const float4 b = *reinterpret_cast<const float4*>(rec + 10);         // byte 80
-        const float4 c = *reinterpret_cast<const float4*>(rec + 12);         // byte 96
-        r.z[0] = a.x; r.z[1] = a.y; r.z[2] = b.x; r.z[3] = b.y;
-        r.z[4] = b.z; r.z[5] = b.w; r.z[6] = c.x; r.z[7] = c.y; r.z[8] = c.z;
-    }
-    static constexpr bool kPipeline = true;
-    __device__ __forceinline__ static bool invalid(const Rec& r) { return r.x[0] != r.x[0]; }  // NaN mark
-    using Q = double;
-    using Aux = int;
-    __device__ __forceinline__ Q pre(const Rec& i, const Rec& j) const {
-        double A = __dmul_rn(i.x[0], j.z[0]);
-        double B = __dmul_rn(i.z[0], j.x[0]);
-#pragma unroll
-        for (int k = 1; k < 9; ++k) {
-            A = __fma_rn(i.x[k], j.z[k], A);
-            B = __fma_rn(i.z[k], j.x[k], B);
-        }
-        return __dadd_rn(A, B);
-    }
-    __device__ __forceinline__ static Aux aux(const Rec&) { return 0; }
-    __device__ __forceinline__ WT post(Q T, const Rec&, Aux) const { return weight_kl<WT>(T, lk); }
-    __device__ __forceinline__ WT weight(const Rec& i, const Rec& j) const {
-        return post(pre(i, j), i, aux(j));
-    }
-};
-
-#ifndef POLSAR_KLF_TY
-#define POLSAR_KLF_TY 24
-#endif
-#ifndef POLSAR_KLF_RB
-#define POLSAR_KLF_RB 2
-#endif
-
-// Backward sums in shared memory (ACC forms of pass 1, window and KL): each
-// pair weight w(i, j) is added to j's backward sum as the fixed-point integer
-// round(w 2^44), split over two 32-bit counters (bits 22 and up, bits 0-21)
-// so the native shared-memory ATOMS.ADD serves: integer addition is exact
-// and associative, so the sums are bit-reproducible in any order and any
-// tiling.  Per target and tile at most 2R(R+1) <= 312 weights <= 1 arrive
-// (positive-definite inputs: d >= 0): the high counter stays below 2^31, and
-// the low one, fed < 2^22 per add, below 2^30.1.  Bit 31 of the low counter
-// is a NaN flag: a pixel marked invalid by the prepass (NaN g or X) sets it on
-// its own slot and on all its forward targets, so W comes out NaN exactly on
-// the pixels whose window holds it (its forward-pair weights are NaN too and
-// make F NaN; the integers they add to flagged slots are discarded).
-constexpr float kFix = 17592186044416.0f;  // 2^44
-constexpr unsigned kBadBit = 0x80000000u;
-constexpr long long kBadSum = (long long)(1ull << 63);  // a flagged tile sum in part[]
-__device__ __forceinline__ long long fixed_w(float w) { return __float2ll_rn(w * kFix); }
-__device__ __forceinline__ long long fixed_w(double w) { return __double2ll_rn(w * (double)kFix); }
-__device__ __forceinline__ void acc_add(unsigned* ah, int hp, int q, long long v) {
-    atomicAdd(ah + q, (unsigned)((unsigned long long)v >> 22));
-    atomicAdd(ah + hp + q, (unsigned)(v & 0x3fffff));
-}
-
-// Pass 1, one full window row (all 2R+1 neighbours valid for every owned
-// row): weights into row[] and, for owned in-image pairs, into the planes
-// wp[r] (advanced by one plane per neighbour), or (ACC) into the neighbours'
-// backward sums ah[qj + wx + R].
-template <typename Pair, int RB, bool FULL, bool ACC>
-__device__ __forceinline__ void fwd_full_row(const Pair& pr, const typename Pair::Rec (&ri)[RB],
-                                             const typename Pair::T* rec, int R, int64_t gx,
-                                             int64_t width, bool interior_x, const bool (&own)[RB],
-                                             typename Pair::WT* (&wp)[RB], int64_t N,
-                                             typename Pair::WT (&row)[RB], unsigned* ah, int hp, int qj) {
-    // FULL: the CTA's whole tile is inside the image and the output rows, so
-    // every pair is in-image and owned: no masks, unconditional stores
-    using WT = typename Pair::WT;
-#pragma unroll kSymUnroll
-    for (int wx = -R; wx <= R; ++wx, rec += Pair::RS, ++qj) {
-        typename Pair::Rec rj;
-        Pair::load(rec, rj);
-        const bool colok = FULL || interior_x || (gx + wx >= 0 && gx + wx < width);
-        long long v = 0;
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            WT w = pr.weight(ri[r], rj);
-            if constexpr (ACC) {
-                if (!FULL) w = colok ? w : WT(0);
-                row[r] += w;
-                if (FULL || own[r]) v += fixed_w(w);
-            } else if constexpr (FULL) {
-                row[r] += w;
-                *wp[r] = w;
-            } else {
-                w = colok ? w : WT(0);
-                row[r] += w;
-                if (colok && own[r]) *wp[r] = w;
-            }
-            if constexpr (!ACC) wp[r] += N;
-        }
-        if constexpr (ACC) acc_add(ah, hp, qj, v);
-    }
-}
-
-// The same row software-pipelined by one neighbour: the FP64 part (pre) of
-// neighbour wx and the weight, sum and store (post) of wx - 1 form one basic
-// block, so the scheduler overlaps them.  The first post is a no-op
-// (ok = false) and the sums keep wx order, so results equal fwd_full_row's.
-template <typename Pair, int RB, bool ACC>
-__device__ __forceinline__ void fwd_full_row_pipelined(
-    const Pair& pr, const typename Pair::Rec (&ri)[RB], const typename Pair::T* rec, int R,
-    int64_t gx, int64_t width, bool interior_x, const bool (&own)[RB], typename Pair::WT* (&wp)[RB],
-    int64_t N, typename Pair::WT (&row)[RB], unsigned* ah, int hp, int qj) {
-    using WT = typename Pair::WT;
-    typename Pair::Q qp[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        wp[r] -= N;
-        qp[r] = typename Pair::Q(1);
-    }
-    typename Pair::Aux ap = Pair::aux(ri[0]);
-    bool okp = false;
-#pragma unroll kSymUnroll
-    for (int wx = -R; wx <= R; ++wx, rec += Pair::RS) {
-        typename Pair::Rec rj;
-        Pair::load(rec, rj);
-        const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-        typename Pair::Q q[RB];
-#pragma unroll
-        for (int r = 0; r < RB; ++r) q[r] = pr.pre(ri[r], rj);
-        long long v = 0;
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            WT w = pr.post(qp[r], ri[r], ap);
-            w = okp ? w : WT(0);
-            row[r] += w;
-            if constexpr (ACC) {
-                if (own[r]) v += fixed_w(w);
-            } else {
-                if (okp && own[r]) *wp[r] = w;
-                wp[r] += N;
-            }
-            qp[r] = q[r];
-        }
-        if constexpr (ACC) {
-            if (wx > -R) acc_add(ah, hp, qj + wx + R - 1, v);  // neighbour wx - 1
-        }
-        ap = Pair::aux(rj);
-        okp = colok;
-    }
-    long long v = 0;
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {  // the last neighbour's post
-        WT w = pr.post(qp[r], ri[r], ap);
-        w = okp ? w : WT(0);
-        row[r] += w;
-        if constexpr (ACC) {
-            if (own[r]) v += fixed_w(w);
-        } else {
-            if (okp && own[r]) *wp[r] = w;
-        }
-    }
-    if constexpr (ACC) acc_add(ah, hp, qj + 2 * R, v);
-}
-
-// Pass 1, generic over the pair policy.  ACC: instead of storing the pair
-// weights, accumulate every in-tile-halo neighbour's backward sum in shared
-// memory (fixed point, acc_add) and write the tile's halo-region sums to
-// part[tile][HP] (int64) at the end; pass 2 (k_window_bwd_acc) adds the <= 4
-// tiles' sums of each pixel.
-template <typename Pair, int TY, int RB, bool ACC = false>
-__global__ void __launch_bounds__(K3_TX * TY / RB, 1)
-k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64_t row_end, int R,
-             int64_t wpitch, typename Pair::WT* __restrict__ wbuf, double* __restrict__ fbuf,
-             long long* __restrict__ part) {
-    using T = typename Pair::T;
-    using WT = typename Pair::WT;
-    using Rec = typename Pair::Rec;
-    constexpr int RS = Pair::RS;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int HW = K3_TX + 2 * R;   // halo columns x0-R .. x0+TX-1+R
-    const int HH = TY + R;          // halo rows y0 .. y0+TY-1+R (forward only)
-    const int HP = HW * HH;
-    T* sz = reinterpret_cast<T*>(smem_raw);  // HP records of RS T
-    const int64_t N = slab_rows * wpitch;    // weight-plane stride (row pitch wpitch >= width)
-
-    const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
-    const int64_t y0 = row_begin + (int64_t)blockIdx.y * TY;
-    // ACC: the backward-sum counters follow the records (high words, then low)
-    unsigned* ah = reinterpret_cast<unsigned*>(sz + (size_t)RS * HP);
-    for (int q = threadIdx.x; q < HP; q += blockDim.x) {
-        int hy = q / HW, hx = q % HW;
-        int64_t gy = y0 + hy, gx = x0 - R + hx;
-        bool in = gy < slab_rows && gx >= 0 && gx < width;
-        pr.fill(sz + RS * q, in ? gy * width + gx : 0, in);
-        if constexpr (ACC) {
-            ah[q] = 0u;
-            ah[HP + q] = 0u;
-        }
-    }
-    __syncthreads();
-
-    const int tx = threadIdx.x % K3_TX;
-    const int ty0 = (threadIdx.x / K3_TX) * RB;
-    const int64_t gx = x0 + tx;
-    Rec ri[RB];
-    double acc[RB];
-    bool own[RB];
-    int64_t pi[RB];  // weight-plane index of the owned pixel (F is indexed gy * width + gx)
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        const int64_t gy = y0 + ty0 + r;
-        own[r] = gx < width && gy < row_end;
-        pi[r] = gy * wpitch + gx;
-        Pair::load(sz + RS * ((ty0 + r) * HW + (tx + R)), ri[r]);
-        acc[r] = 0.0;
-    }
-    const bool interior_x = (x0 - R >= 0) && (x0 + K3_TX + R <= width);
-    const bool full = interior_x && y0 + TY <= row_end;  // CTA-uniform
-    if constexpr (ACC) {
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            if (own[r] && Pair::invalid(ri[r])) {  // rare: flag the pixel and its forward targets
-                const int q0 = (ty0 + r) * HW + (tx + R);
-                atomicOr(ah + HP + q0, kBadBit);
-                for (int dy = 0; dy <= R; ++dy)
-                    for (int dx = (dy == 0 ? 1 : -R); dx <= R; ++dx)
-                        atomicOr(ah + HP + q0 + dy * HW + dx, kBadBit);
-            }
-        }
-    }
-
-    for (int wy = 0; wy <= R + RB - 1; ++wy) {
-        const int64_t gyj = y0 + ty0 + wy;
-        if (gyj >= slab_rows) break;  // warp-uniform
-        const int hy = ty0 + wy;
-        const T* rec = sz + RS * (hy * HW + tx);  // neighbour wx = -R
-        WT row[RB];
-#pragma unroll
-        for (int r = 0; r < RB; ++r) row[r] = WT(0);
-        if (wy >= RB && wy <= R) {
-            // every owned pixel sees this row at dy = wy - r in [1, R]: full rows.
-            // wp[r] walks the weight planes delta = (wy - r, wx), consecutive in wx.
-            WT* wp[RB];
-#pragma unroll
-            for (int r = 0; r < RB; ++r) wp[r] = wbuf + (int64_t)fwd_index(wy - r, -R, R) * N + pi[r];
-            POLSAR_CHECK(hy >= 0 && hy < HH && tx + 2 * R < HW);  // records wx = -R..R
-            const int qj = hy * HW + tx;  // backward-sum slot of neighbour wx = -R
-            if constexpr (Pair::kPipeline)
-                fwd_full_row_pipelined<Pair, RB, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row,
-                                                      ah, HP, qj);
-            else if (full)
-                fwd_full_row<Pair, RB, true, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row,
-                                                  ah, HP, qj);
-            else
-                fwd_full_row<Pair, RB, false, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row,
-                                                   ah, HP, qj);
-        } else {
-            for (int wx = -R; wx <= R; ++wx, rec += RS) {
-                POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-                Rec rj;
-                Pair::load(rec, rj);
-                const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-                long long v = 0;
-#pragma unroll
-                for (int r = 0; r < RB; ++r) {
-                    const int dy = wy - r;
-                    if (dy >= 0 && dy <= R && (dy > 0 || wx > 0)) {  // warp-uniform
-                        WT w = pr.weight(ri[r], rj);
-                        w = colok ? w : WT(0);
-                        row[r] += w;
-                        if constexpr (ACC) {
-                            if (own[r]) v += fixed_w(w);
-                        } else {
-                            if (colok && own[r]) wbuf[(int64_t)fwd_index(dy, wx, R) * N + pi[r]] = w;
-                        }
-                    }
-                }
-                if constexpr (ACC) acc_add(ah, HP, hy * HW + tx + wx + R, v);
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < RB; ++r) acc[r] += (double)row[r];
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r)
-        if (gx < width && y0 + ty0 + r < row_end) fbuf[(y0 + ty0 + r) * width + gx] = acc[r];
-    if constexpr (ACC) {
-        __syncthreads();
-        long long* dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * HP;
-        for (int q = threadIdx.x; q < HP; q += blockDim.x) {
-            const unsigned lo = ah[HP + q];
-            dst[q] = (lo & kBadBit) ? kBadSum : (long long)(((unsigned long long)ah[q] << 22) + lo);
-        }
-    }
-}
-
-// Pass 2 of the ACC forms: W_j = 1 + F_j + 2^-44 (sum of the backward sums of
-// the <= 4 pass-1 tiles whose halo region holds j; integer, exact).  Tile
-// (bx, by) covers rows p0 + by TY .. + TY + R - 1 and columns 32 bx - R ..
-// 32 bx + 31 + R of its halo region.
-template <typename S>
-__global__ void __launch_bounds__(256)
-k_window_bwd_acc(const long long* __restrict__ part, const double* __restrict__ fbuf, int64_t width,
-                 int64_t row_begin, int64_t row_end, int64_t p0, int R, int TY, int nbx, int nby,
-                 S* __restrict__ out) {
-    const int HW = K3_TX + 2 * R;
-    const int HP = HW * (TY + R);
-    const int64_t m = (row_end - row_begin) * width;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t y = row_begin + q / width, x = q % width;
-        const int64_t yr = y - p0;  // >= 0
-        // by: p0 + by TY <= y < p0 + by TY + TY + R ; bx: 32 bx - R <= x < 32 bx + 32 + R
-        const int64_t by_hi = yr / TY;
-        const int64_t by_lo = yr - TY - R + 1 > 0 ? (yr - TY - R + 1 + TY - 1) / TY : 0;
-        const int64_t bx_hi = (x + R) / K3_TX < nbx - 1 ? (x + R) / K3_TX : nbx - 1;
-        const int64_t bx_lo = x - K3_TX - R + 1 > 0 ? (x - K3_TX - R + 1 + K3_TX - 1) / K3_TX : 0;
-        long long sum = 0;
-        bool bad = false;
-        for (int64_t by = by_lo; by <= by_hi && by < nby; ++by)
-            for (int64_t bx = bx_lo; bx <= bx_hi; ++bx) {
-                const int64_t hy = yr - by * TY, hx = x - K3_TX * bx + R;
-                POLSAR_CHECK(hy >= 0 && hy < TY + R && hx >= 0 && hx < HW);
-                const long long t = part[(by * nbx + bx) * HP + hy * HW + hx];
-                bad = bad || t == kBadSum;
-                sum += t;
-            }
-        const double wb = bad ? __longlong_as_double(0x7ff8000000000000ll) : (double)sum * (1.0 / (double)kFix);
-        out[q] = (S)__dadd_rn(__dadd_rn(1.0, fbuf[y * width + x]), wb);
-    }
-}
-
-// Pass 2: W_j = 1 + F_j + sum over backward neighbours, one thread per pixel.
-// Each (delta_y) row of weights is summed in WT, then added in double.  RC > 0
-// fixes R at compile time (the paper's R = 11), so a row's 2R+1 independent
-// loads are all in flight at once.
-template <typename S, typename WT, int RC>
-__global__ void __launch_bounds__(256)
-k_window_bwd(const WT* __restrict__ wbuf, const double* __restrict__ fbuf, int64_t width,
-             int64_t wpitch, int64_t slab_rows, int64_t row_begin, int64_t row_end, int R_rt,
-             S* __restrict__ out) {
-    const int R = RC > 0 ? RC : R_rt;
-    const int64_t N = slab_rows * wpitch;  // weight-plane stride
-    const int64_t m = (row_end - row_begin) * width;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t y = row_begin + q / width, x = q % width;
-        const int64_t p = y * width + x;
-        double acc = 1.0 + fbuf[p];
-        const bool inx = x - R >= 0 && x + R < width;
-        for (int dy = 0; dy <= R; ++dy) {
-            if (y - dy < 0) break;
-            const int dx0 = dy == 0 ? 1 : -R;
-            const WT* base = wbuf + (int64_t)fwd_index(dy, dx0, R) * N + (y - dy) * wpitch + x - dx0;
-            WT rowp = WT(0);
-            if (inx) {
-                if (RC > 0 && dy > 0) {
-#pragma unroll
-                    for (int k = 0; k < 2 * RC + 1; ++k) rowp += base[(int64_t)k * (N - 1)];
-                } else {
-                    for (int dx = dx0; dx <= R; ++dx) rowp += base[(int64_t)(dx - dx0) * (N - 1)];
-                }
-            } else {
-                for (int dx = dx0; dx <= R; ++dx)
-                    if (x - dx >= 0 && x - dx < width) rowp += base[(int64_t)(dx - dx0) * (N - 1)];
-            }
-            acc += (double)rowp;
-        }
-        out[q] = (S)acc;
-    }
-}
-
-template <typename Pair>
-size_t window_fwd_smem(int TY, int R) {
-    return (size_t)(K3_TX + 2 * R) * (TY + R) * Pair::RS * sizeof(typename Pair::T);
-}
-
-// Launch pass 1 over rows [p0, re) (p0 = max(0, rb - R): the R rows above the
-// output rows hold the forward pairs that are their backward pairs).
-// Pass-1 tile grid over rows [p0, re): (nbx, nby) and the halo-region size
-// HP of a tile (also the ACC forms' backward-sum slots per tile).
-struct FwdGrid {
-    int64_t p0;
-    int nbx, nby, HP;
-};
-inline FwdGrid fwd_grid(int64_t width, int64_t rb, int64_t re, int R, int TY) {
-    FwdGrid g;
-    g.p0 = rb - R > 0 ? rb - R : 0;
-    g.nbx = (int)((width + K3_TX - 1) / K3_TX);
-    g.nby = (int)((re - g.p0 + TY - 1) / TY);
-    g.HP = (K3_TX + 2 * R) * (TY + R);
-    return g;
-}
-
-template <typename Pair, int TY, int RB, bool ACC = false>
-int launch_fwd(const Pair& pr, int64_t width, int64_t slab_rows, int64_t rb, int64_t re, int R,
-               typename Pair::WT* wbuf, double* fbuf, cudaStream_t s, const char* who,
-               long long* part = nullptr) {
-    const FwdGrid fg = fwd_grid(width, rb, re, R, TY);
-    const size_t smem = window_fwd_smem<Pair>(TY, R) + (ACC ? 2 * sizeof(unsigned) * (size_t)fg.HP : 0);
-    auto kern = k_window_fwd<Pair, TY, RB, ACC>;
-    if (smem > K3_SMEM_MAX ||
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return fail(POLSAR_ENOTSUP, who);
-    dim3 grid((unsigned)fg.nbx, (unsigned)fg.nby);
-    kern<<<grid, K3_TX * TY / RB, smem, s>>>(pr, width, slab_rows, fg.p0, re, R, weight_pitch<typename Pair::WT>(width),
-                                             wbuf, fbuf, part);
-    return POLSAR_OK;
-}
-
-// shared memory of pass 1 in the ACC form (records + two counters per slot)
-template <typename Pair>
-size_t acc_fwd_smem(int TY, int R) {
-    return window_fwd_smem<Pair>(TY, R) + 2 * sizeof(unsigned) * (size_t)(K3_TX + 2 * R) * (TY + R);
-}
-
-template <typename S>
-void launch_bwd_acc(const long long* part, const double* fbuf, int64_t width, int64_t rb, int64_t re,
-                    int R, int TY, void* outv, cudaStream_t s) {
-    const FwdGrid fg = fwd_grid(width, rb, re, R, TY);
-    k_window_bwd_acc<S><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(part, fbuf, width, rb, re, fg.p0, R,
-                                                                        TY, fg.nbx, fg.nby, (S*)outv);
-}
-
-// workspace of the ACC forms: the prepass planes (pre_bytes) | F | the tiles'
-// backward sums (int64, HP per tile, over the whole slab's row range)
-inline size_t acc_sym_bytes(size_t pre_bytes, int64_t slab_rows, int64_t width, int R, int TY) {
-    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-    const FwdGrid fg = fwd_grid(width, 0, slab_rows, R, TY);
-    return up(pre_bytes) + up((size_t)slab_rows * width * sizeof(double)) +
-           up((size_t)fg.nbx * fg.nby * fg.HP * sizeof(long long));
-}
-
-// Window / KL symmetric form: backward sums in shared memory (ACC, default)
-// or through the weight planes (POLSAR_WINDOW_PLANES=1, the A/B alternative).
-bool window_planes() {
-    static const bool v = [] {
-        const char* e = getenv("POLSAR_WINDOW_PLANES");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
-
-template <typename S, typename WT>
-void launch_bwd(const WT* wbuf, const double* fbuf, int64_t width, int64_t slab_rows, int64_t rb,
-                int64_t re, int R, void* outv, cudaStream_t s) {
-    if (R == 11)
-        k_window_bwd<S, WT, 11><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
-            wbuf, fbuf, width, weight_pitch<WT>(width), slab_rows, rb, re, R, (S*)outv);
-    else
-        k_window_bwd<S, WT, 0><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(
-            wbuf, fbuf, width, weight_pitch<WT>(width), slab_rows, rb, re, R, (S*)outv);
-}
-
-// workspace: g (N x WT) | F (N x double) | wbuf (fwd_count(R) weight planes
-// of slab_rows x weight_pitch(width) WT; see weight_pitch)
-template <typename WT>
-size_t window_sym_bytes(int64_t slab_rows, int64_t width, int R) {
-    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-    const int64_t n = slab_rows * width;
-    return up(n * sizeof(WT)) + up(n * sizeof(double)) +
-           up((size_t)fwd_count(R) * slab_rows * weight_pitch<WT>(width) * sizeof(WT));
-}
-
-template <typename S, typename T, typename WT>
-int launch_window_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                      int64_t re, int R, double looks, double h, void* wsv, void* outv,
-                      cudaStream_t s) {
-    const S* z = (const S*)zv;
-    const int64_t n = slab_rows * width;
-    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-    unsigned char* ws = (unsigned char*)wsv;
-    WT* g = (WT*)ws;
-    double* fbuf = (double*)(ws + up(n * sizeof(WT)));
-    WT* wbuf = (WT*)(ws + up(n * sizeof(WT)) + up(n * sizeof(double)));
-    k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
-    const double alpha = looks / (2.0 * h);
-    const char* who = "polsar_window_distance: shared memory request too large";
-    if (!window_planes() && acc_fwd_smem<LogDetPair<S, T, WT, 1>>(POLSAR_SYM_TY, R) <= K3_SMEM_MAX) {
-        long long* part = (long long*)wbuf;  // (same offset: g | F | tile sums)
-        int rc = alpha == 2.0
-                     ? launch_fwd<LogDetPair<S, T, WT, 1>, POLSAR_SYM_TY, POLSAR_SYM_RB, true>(
-                           LogDetPair<S, T, WT, 1>{z, ld, g, (WT)alpha, true}, width, slab_rows, rb, re, R,
-                           nullptr, fbuf, s, who, part)
-                     : launch_fwd<LogDetPair<S, T, WT, 0>, POLSAR_SYM_TY, POLSAR_SYM_RB, true>(
-                           LogDetPair<S, T, WT, 0>{z, ld, g, (WT)alpha, false}, width, slab_rows, rb, re, R,
-                           nullptr, fbuf, s, who, part);
-        if (rc != POLSAR_OK) return rc;
-        launch_bwd_acc<S>(part, fbuf, width, rb, re, R, POLSAR_SYM_TY, outv, s);
-        return launch_check("polsar_window_distance: launch failed");
-    }
-    int rc = alpha == 2.0
-                 ? launch_fwd<LogDetPair<S, T, WT, 1>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
-                       LogDetPair<S, T, WT, 1>{z, ld, g, (WT)alpha, true}, width, slab_rows, rb, re, R,
-                       wbuf, fbuf, s, who)
-                 : launch_fwd<LogDetPair<S, T, WT, 0>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
-                       LogDetPair<S, T, WT, 0>{z, ld, g, (WT)alpha, false}, width, slab_rows, rb, re, R,
-                       wbuf, fbuf, s, who);
-    if (rc != POLSAR_OK) return rc;
-    launch_bwd<S, WT>(wbuf, fbuf, width, slab_rows, rb, re, R, outv, s);
-    return launch_check("polsar_window_distance: launch failed");
-}
-
-// K6, symmetric form: the KL prepass planes | F | weight planes.
-template <typename WT>
-size_t kl_sym_bytes(int64_t slab_rows, int64_t width, int R) {
-    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-    const int64_t n = slab_rows * width;
-    return up((size_t)n * V3_NP * sizeof(double)) + up(n * sizeof(double)) +
-           up((size_t)fwd_count(R) * slab_rows * weight_pitch<WT>(width) * sizeof(WT));
-}
-
-template <typename S, typename WT>
-int launch_window_kl_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                         int64_t re, int R, double looks, double h, void* wsv, void* outv,
-                         cudaStream_t s) {
-    const int64_t n = slab_rows * width;
-    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-    unsigned char* ws = (unsigned char*)wsv;
-    double* prep = (double*)ws;
-    double* fbuf = (double*)(ws + up((size_t)n * V3_NP * sizeof(double)));
-    WT* wbuf = (WT*)(ws + up((size_t)n * V3_NP * sizeof(double)) + up(n * sizeof(double)));
-    k_window_prep_kl<S><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, prep);
-    KLPair<WT> pr{prep, n, (WT)(looks / h)};
-    if constexpr (sizeof(S) == 4) {  // fp32 storage: the 112-byte records
-        constexpr int TYF = POLSAR_KLF_TY;
-        KLPairF<WT> pf{prep, n, (WT)(looks / h)};
-        if (!window_planes() && acc_fwd_smem<KLPairF<WT>>(TYF, R) <= K3_SMEM_MAX) {
-            long long* part = (long long*)wbuf;
-            int rc = launch_fwd<KLPairF<WT>, TYF, POLSAR_KLF_RB, true>(pf, width, slab_rows, rb, re, R, nullptr, fbuf, s,
-                                                            "polsar_window_kl: shared memory request too large",
-                                                            part);
-            if (rc != POLSAR_OK) return rc;
-            launch_bwd_acc<S>(part, fbuf, width, rb, re, R, TYF, outv, s);
-            return launch_check("polsar_window_kl: launch failed");
-        }
-    }
-    // (KL at R = 12: records + counters exceed shared memory; the plane form serves)
-    if (!window_planes() && acc_fwd_smem<KLPair<WT>>(16, R) <= K3_SMEM_MAX) {
-        long long* part = (long long*)wbuf;
-        int rc = launch_fwd<KLPair<WT>, 16, 2, true>(pr, width, slab_rows, rb, re, R, nullptr, fbuf, s,
-                                                      "polsar_window_kl: shared memory request too large", part);
-        if (rc != POLSAR_OK) return rc;
-        launch_bwd_acc<S>(part, fbuf, width, rb, re, R, 16, outv, s);
-        return launch_check("polsar_window_kl: launch failed");
-    }
-    int rc = launch_fwd<KLPair<WT>, 16, 2>(pr, width, slab_rows, rb, re, R, wbuf, fbuf, s,
-                                            "polsar_window_kl: shared memory request too large");
-    if (rc != POLSAR_OK) return rc;
-    launch_bwd<S, WT>(wbuf, fbuf, width, slab_rows, rb, re, R, outv, s);
-    return launch_check("polsar_window_kl: launch failed");
-}
-
-// ------------------------------------------------------------------------
-// K4, symmetric form (default for R <= V3_RMAX): pass 1 (k_window_fwd with
-// the log-det pair policy) stores every unordered pair's weight once; this
-// gather pass then forms, for every output pixel i,
-//   W_i = sum_j w_ij,   Zhat_i = sum_j w_ij Z_j / W_i
-// reading w_ij from the weight planes: with j = i + (dy, dx),
-//   forward  (dy > 0, or dy = 0 and dx > 0): w_ij = wbuf[fwd_index(dy, dx)][i]
-//   backward (the mirror):                   w_ij = wbuf[fwd_index(-dy, -dx)][j]
-//   j = i:                                   w_ii = 1 (d_ii = 0)
-// Along a neighbour row both offsets are linear in dx: forward
-// fwd_index(dy, 0) N + i + dx N, backward fwd_index(-dy, 0) N + j0 + dx (1 - N)
-// (j0 = the neighbour at dx = 0; for dy = 0, fwd_index(0, 0) = -1 and j0 = i).
-// So the pass is pure data movement plus 9 FMAs per ordered pair in the
-// storage precision: no FP64 determinant work at all (the direct form
-// k_nlm_sum evaluates every ordered pair's determinant, 29 FP64 ops, plus 10
-// FP64 accumulations).
-//
-// A CTA owns NLM_COLS = NLM_TX - AL columns x RB rows (AL = 16 / sizeof(WT));
-// each thread one column and RB rows, and the CTA walks the window rows its
-// pixels share.  For each window row:
-//  * the weights: for every owned row r and dx, the CTA's weights form one
-//    contiguous run of a weight plane (at i for forward pairs, at j = i +
-//    (dy, dx) for backward ones), fetched by TMA as one 1-D tile of NLM_TX
-//    elements of a tensor map over the whole weight buffer.  TMA needs a
-//    16-byte aligned start (measured, tools/micro/tma1d_test.cu); with the
-//    padded plane layout (weight_pitch) forward runs start aligned and a
-//    backward run at dx starts m(dx) = dx mod AL elements past an aligned
-//    point, so its tile is fetched from there and read at offset m(dx).
-//    Tiles of rows that do not pair with this window row, and the j = i
-//    tile, are fetched from an out-of-range coordinate: TMA zero-fills them.
-//    RB (2R + 1) tiles per row, one per thread, completing on the stage's
-//    mbarrier; NLM_NS row stages in flight.
-//  * the neighbours Z_j: the row's 9 planes over NLM_TX + 2 V3_RMAX columns
-//    (zero-filled outside the image), staged by cp.async into a ring of
-//    NLM_NZ rows; each Z_j is read from shared memory once per thread and
-//    serves its RB pairs.
-// Window rows above the owned rows are all-backward, rows below all-forward
-// (fully unrolled, branch-free); the RB rows in between mix both laws and
-// the self pair, whose w_ii = 1 is added after the row.  Columns within R of
-// the image edge mask the out-of-image pairs.  Shared-memory reads are
-// conflict-free (consecutive lanes, consecutive columns).  Per window row the
-// pairs are summed in WT (2R + 1 terms), then added to fp64 totals in a fixed
-// order per pixel: bit-reproducible, and slab decompositions are exact.
-#ifndef POLSAR_NLM_RB
-#define POLSAR_NLM_RB 2
-#endif
-#ifndef POLSAR_NLM_NS
-#define POLSAR_NLM_NS 2
-#endif
-constexpr int NLM_TX = 128;                    // threads per CTA = TMA tile length
-constexpr int NLM_NZ = 3;                      // Z row buffers
-constexpr int NLM_ZW = NLM_TX + 2 * V3_RMAX;   // staged Z columns x0 - 12 .. x0 + 139
-// Z record of one staged column: the 9 planes padded to 16-byte vectors
-// (12 floats / 10 doubles; strides of 12 and 20 words keep the 16-byte
-// loads of 8 consecutive lanes on distinct banks)
-template <typename S>
-#ifndef POLSAR_NLM_REC9
-#define POLSAR_NLM_REC9 1
-#endif
-struct NlmRec {
-    // (POLSAR_NLM_REC9: fp32 records unpadded, 9 words, read as 9 scalars)
-    static constexpr int n = sizeof(S) == 4 ? (POLSAR_NLM_REC9 ? 9 : 12) : 10;
-};
-constexpr int NLM_OOB = -(1 << 30);            // a TMA coordinate whose tile is all zero-fill
-
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
-    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    int src_bytes = valid ? 4 : 0;  // 0: zero-fill
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(sa), "l"(gmem), "r"(src_bytes)
-                 : "memory");
-}
-
-// stage window row gy (9 planes, columns x0 - V3_RMAX .. x0 + NLM_TX + V3_RMAX - 1)
-template <typename S>
-__device__ __forceinline__ void nlm_stage_row(S* dst, const S* __restrict__ z, int64_t ld,
-                                              int64_t width, int64_t gy, int64_t x0) {
-    const S* src = z + gy * width;
-    constexpr int ZR = NlmRec<S>::n;
-    for (int c = threadIdx.x; c < NLM_ZW; c += NLM_TX) {
-        const int64_t gx = x0 - V3_RMAX + c;
-        const bool ok = gx >= 0 && gx < width;
-        const S* sp = src + (ok ? gx : 0);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            if constexpr (sizeof(S) == 4)
-                cp_async4(dst + c * ZR + k, sp + k * ld, ok);
-            else
-                cp_async8(dst + c * ZR + k, sp + k * ld, ok);
-        }
-    }
-}
-
-template <int AL>
-__host__ __device__ __forceinline__ int nlm_mis(int wx) { return wx & (AL - 1); }
-
-// TMA coordinates (pixel index within the plane, a multiple of AL; plane)
-// of the tile of owned row yi at dx for window row gy; plane NLM_OOB when
-// the row does not pair (the tile zero-fills).
-template <int AL>
-__device__ __forceinline__ int2 nlm_tile_coord(int64_t gy, int64_t yi, int wx, int R, int64_t wp,
-                                               int64_t x0, int64_t row_end) {
-    const int64_t dy = gy - yi;
-    if (yi >= row_end || dy < -R || dy > R || (dy == 0 && wx == 0)) return make_int2(0, NLM_OOB);
-    const int ad = (int)(dy < 0 ? -dy : dy);
-    const int fi = ad == 0 ? -1 : R + (ad - 1) * (2 * R + 1) + R;  // fwd_index(|dy|, 0)
-    if (dy > 0 || (dy == 0 && wx > 0)) return make_int2((int)(yi * wp + x0), fi + wx);  // forward: at i
-    return make_int2((int)(gy * wp + x0 + wx - nlm_mis<AL>(wx)), fi - wx);           // backward: at j
-}
-
-template <typename WT>
-size_t nlm_smem_bytes(int R, int RB, int NS, size_t s_bytes) {
-    return 128 + (size_t)NS * RB * (2 * R + 1) * NLM_TX * sizeof(WT) +
-           (size_t)NLM_NZ * NLM_ZW * (s_bytes == 4 ? NlmRec<float>::n : NlmRec<double>::n) * s_bytes;
-}
-
-// One window row for one thread: K = 0 all rows backward, 1 all forward,
-// 2 mixed (cls[r]: 0 backward, 1 forward, 2 the pixel's own row, backward for
-// dx < 0 and forward for dx > 0; its dx = 0 tile is zero); EDGE masks
-// out-of-image columns.
-__device__ __forceinline__ void nlm_load_rec(const float* p, float (&zj)[9]) {
-#if POLSAR_NLM_REC9
-#pragma unroll
-    for (int k = 0; k < 9; ++k) zj[k] = p[k];
-#else
-    const float4 a = reinterpret_cast<const float4*>(p)[0];
-    const float4 b = reinterpret_cast<const float4*>(p)[1];
-    zj[0] = a.x; zj[1] = a.y; zj[2] = a.z; zj[3] = a.w;
-    zj[4] = b.x; zj[5] = b.y; zj[6] = b.z; zj[7] = b.w;
-    zj[8] = p[8];
-#endif
-}
-__device__ __forceinline__ void nlm_load_rec(const double* p, double (&zj)[9]) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const double2 v = reinterpret_cast<const double2*>(p)[k];
-        zj[2 * k] = v.x;
-        zj[2 * k + 1] = v.y;
-    }
-    zj[8] = p[8];
-}
-
-#ifndef POLSAR_NLM_UNROLL
-#define POLSAR_NLM_UNROLL 4
-#endif
-constexpr int kNlmUnroll = POLSAR_NLM_UNROLL;
-template <typename WT, int AL, int RB, int K, bool EDGE, int RC>
-__device__ __forceinline__ void nlm_row(const WT* __restrict__ wrow, const WT* __restrict__ zrowT, int R,
-                                        const int (&cls)[RB], int64_t x, int64_t width, WT (&pw)[RB],
-                                        WT (&pz)[RB][9]) {
-    // wrow: w(r, dx) tile at wrow[(r * (2R + 1) + dx) * NLM_TX] (+ m(dx) for backward tiles)
-    // zrowT: the record of Z_j(dx) at zrowT + dx * ZR
-    // (a rolled loop: the per-dx body is 9 + RB loads and 10 RB FMA/adds; a
-    // fully unrolled row measured slower, instruction-fetch bound)
-    const int WX = RC > 0 ? 2 * RC + 1 : 2 * R + 1;
-    constexpr int ZR = NlmRec<WT>::n;
-    const WT* zp = zrowT - R * ZR;
-    const WT* wp = wrow - R * NLM_TX;
-#pragma unroll(kNlmUnroll)
-    for (int wx = -R; wx <= R; ++wx, zp += ZR, wp += NLM_TX) {
-        WT zj[9];
-        nlm_load_rec(zp, zj);
-        const bool colok = !EDGE || (x + wx >= 0 && x + wx < width);
-        const int m = nlm_mis<AL>(wx);
-        const WT* wpm = wp + (K == 1 ? 0 : m);
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            const WT* a;
-            if constexpr (K == 2)
-                a = (cls[r] == 0 || (cls[r] == 2 && wx < 0)) ? wpm : wp;
-            else
-                a = wpm;
-            WT w = a[r * WX * NLM_TX];
-            if constexpr (EDGE) w = colok ? w : WT(0);
-            pw[r] = ADD(pw[r], w);
-#pragma unroll
-            for (int k = 0; k < 9; ++k) pz[r][k] = FMA(w, zj[k], pz[r][k]);
-        }
-    }
-}
-
-template <typename S, typename WT, int RC, int RB, int NS>
-__global__ void __launch_bounds__(NLM_TX)
-k_nlm_gather(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap wmap2,
-             const S* __restrict__ z, int64_t ld,
-             int64_t width, int64_t slab_rows, int64_t row_begin, int64_t row_end, int R_rt,
-             S* __restrict__ out_w, S* __restrict__ out_z, int64_t ld_out) {
-    constexpr int AL = 16 / sizeof(WT);
-    constexpr int COLS = NLM_TX - AL;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int R = RC > 0 ? RC : R_rt;
-    const int WX = 2 * R + 1;
-    const int SW = RB * WX * NLM_TX;  // weights per stage
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-    WT* wst = reinterpret_cast<WT*>(smem_raw + 128);
-    S* zs = reinterpret_cast<S*>(smem_raw + 128 + (size_t)NS * SW * sizeof(WT));
-    const CUtensorMap* pmap = &wmap;
-    const CUtensorMap* pmap2 = &wmap2;
-    constexpr int ZREC = NLM_ZW * NlmRec<S>::n;  // one staged row
-
-    const int64_t wp = weight_pitch<WT>(width);
-    const int64_t x0 = (int64_t)blockIdx.x * COLS;
-    const int tx = threadIdx.x;
-    const int64_t x = x0 + tx;
-    const int64_t y0 = row_begin + (int64_t)blockIdx.y * RB;
-    const bool colin = tx < COLS && x < width;  // (other threads still stage rows)
-    const bool inx = x - R >= 0 && x + R < width;
-    const int64_t ga = y0 - R > 0 ? y0 - R : 0;
-    const int64_t gb = (y0 + RB - 1 + R) < slab_rows - 1 ? (y0 + RB - 1 + R) : slab_rows - 1;
-    const int nrows = (int)(gb - ga + 1);
-
-    if (tx == 0) {
-        for (int st = 0; st < NS; ++st) mbar_init(&bar[st], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // weights of window row q -> stage q % NS: thread t fetches tile t = (r, dx)
-    auto issue = [&](int q) {
-        const int64_t gy = ga + q;
-        const int st = q % NS;
-        if (tx == 0) mbar_expect_tx(&bar[st], (uint32_t)(SW * sizeof(WT)));
-        for (int t = tx; t < RB * WX; t += NLM_TX) {
-            const int r = t / WX, wx = t - r * WX - R;
-            const int64_t yi = y0 + r, dy = gy - yi;
-            if (yi >= row_end || dy < -R || dy > R || dy > 0) {
-                // a whole forward row (the 2R + 1 planes fwd_index(dy, -R..R) at i: one
-                // 2-D box), or a row that does not pair (one out-of-range box: zeros)
-                if (wx == -R) {
-                    const bool act = yi < row_end && dy >= -R && dy <= R;
-                    const int c0 = act ? (int)(yi * wp + x0) : 0;
-                    const int c1 = act ? R + (int)(dy - 1) * (2 * R + 1) : NLM_OOB;
-                    tma_load_2d(wst + (size_t)st * SW + (size_t)t * NLM_TX, pmap2, c0, c1, &bar[st]);
-                }
-            } else {
-                const int2 c = nlm_tile_coord<AL>(gy, yi, wx, R, wp, x0, row_end);
-                tma_load_2d(wst + (size_t)st * SW + (size_t)t * NLM_TX, pmap, c.x, c.y, &bar[st]);
-            }
-        }
-    };
-#pragma unroll
-    for (int q = 0; q < NS - 1; ++q)
-        if (q < nrows) issue(q);
-#pragma unroll
-    for (int q = 0; q < NLM_NZ - 1; ++q) {
-        if (q < nrows) nlm_stage_row<S>(zs + (size_t)q * ZREC, z, ld, width, ga + q, x0);
-        cp_async_commit();
-    }
-
-    double tw[RB], tz[RB][9];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        tw[r] = 0.0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) tz[r][k] = 0.0;
-    }
-    for (int q = 0; q < nrows; ++q) {
-        const int64_t gy = ga + q;
-        // refill the stage and ring slot row q - 1 used (released by the barrier that ended it)
-        if (q + NS - 1 < nrows) issue(q + NS - 1);
-        if (q + NLM_NZ - 1 < nrows)
-            nlm_stage_row<S>(zs + (size_t)((q + NLM_NZ - 1) % NLM_NZ) * ZREC, z, ld, width,
-                             gy + NLM_NZ - 1, x0);
-        cp_async_commit();
-        cp_async_wait<NLM_NZ - 1>();
-        __syncthreads();
-        mbar_wait(&bar[q % NS], (uint32_t)((q / NS) & 1));
-        if (colin) {
-            // records dx = -R..R of column tx, and tile elements tx + m(dx) (m < AL)
-            POLSAR_CHECK(tx + V3_RMAX - R >= 0 && tx + V3_RMAX + R < NLM_ZW && tx + AL - 1 < NLM_TX);
-            const S* zrow = zs + (size_t)(q % NLM_NZ) * ZREC + (tx + V3_RMAX) * NlmRec<S>::n;
-            const WT* wrow = wst + (size_t)(q % NS) * SW + tx + R * NLM_TX;
-            WT pw[RB], pz[RB][9];
-#pragma unroll
-            for (int r = 0; r < RB; ++r) {
-                pw[r] = WT(0);
-#pragma unroll
-                for (int k = 0; k < 9; ++k) pz[r][k] = WT(0);
-            }
-            int cls[RB];
-#pragma unroll
-            for (int r = 0; r < RB; ++r) cls[r] = gy < y0 + r ? 0 : (gy > y0 + r ? 1 : 2);
-            const int K = gy < y0 ? 0 : (gy >= y0 + RB ? 1 : 2);  // CTA-uniform
-            static_assert(sizeof(S) == sizeof(WT), "the gather reads Z in the weight type");
-            const WT* zr = reinterpret_cast<const WT*>(zrow);
-            if (inx) {
-                if (K == 0) nlm_row<WT, AL, RB, 0, false, RC>(wrow, zr, R, cls, x, width, pw, pz);
-                else if (K == 1) nlm_row<WT, AL, RB, 1, false, RC>(wrow, zr, R, cls, x, width, pw, pz);
-                else nlm_row<WT, AL, RB, 2, false, RC>(wrow, zr, R, cls, x, width, pw, pz);
-            } else {
-                if (K == 0) nlm_row<WT, AL, RB, 0, true, RC>(wrow, zr, R, cls, x, width, pw, pz);
-                else if (K == 1) nlm_row<WT, AL, RB, 1, true, RC>(wrow, zr, R, cls, x, width, pw, pz);
-                else nlm_row<WT, AL, RB, 2, true, RC>(wrow, zr, R, cls, x, width, pw, pz);
-            }
-#pragma unroll
-            for (int r = 0; r < RB; ++r) {
-                if (gy == y0 + r && y0 + r < row_end) {  // the self pair: w_ii = 1 (d_ii = 0)
-                    pw[r] = ADD(pw[r], WT(1));
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) pz[r][k] = ADD(pz[r][k], zr[k]);
-                }
-                // a row that does not pair with this window row ran on zero weights
-                // but its Z (0 * NaN): skip it
-                const int64_t dyr = gy - (y0 + r);
-                if (y0 + r < row_end && dyr >= -R && dyr <= R) {
-                    tw[r] = __dadd_rn(tw[r], (double)pw[r]);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) tz[r][k] = __dadd_rn(tz[r][k], (double)pz[r][k]);
-                }
-            }
-        }
-        __syncthreads();  // stage q % NS and ring slot q % NLM_NZ are refilled from row q + 1
-    }
-    if (!colin) return;
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        const int64_t yi = y0 + r;
-        if (yi < row_end) {
-            const int64_t o = (yi - row_begin) * width + x;
-            if (out_w) out_w[o] = (S)tw[r];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) out_z[k * ld_out + o] = (S)__ddiv_rn(tz[r][k], tw[r]);
-        }
-    }
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        return (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-                q == cudaDriverEntryPointSuccess)
-                   ? (PFN_cuTensorMapEncodeTiled_v12000)p
-                   : nullptr;
-    }();
-    return fn;
-}
-
-// 2-D view of the weight planes (P x planes, row stride P) with a box of
-// NLM_TX x rows: rows = 1 for single tiles, 2R + 1 for a forward row's
-// consecutive planes in one transfer.  False if the driver call is
-// unavailable or refuses.  (A 1-D map over the flattened buffer also works
-// but caps the buffer at 2^31 elements of 32-bit coordinates.)
-template <typename WT>
-bool nlm_weight_map2(CUtensorMap* m, const WT* wbuf, int64_t P, int planes, int rows) {
-    auto enc = tensor_map_encoder();
-    if (!enc) return false;
-    cuuint64_t dim[2] = {(cuuint64_t)P, (cuuint64_t)planes};
-    cuuint64_t st[1] = {(cuuint64_t)P * sizeof(WT)};
-    cuuint32_t box[2] = {(cuuint32_t)NLM_TX, (cuuint32_t)rows};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(m, sizeof(WT) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
-                     (void*)wbuf, dim, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-template <typename S, typename T, typename WT>
-int launch_nlm_sym(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                   int64_t re, int R, double looks, double h, void* wsv, void* out_w, void* out_z,
-                   int64_t ld_out, cudaStream_t s) {
-    const S* z = (const S*)zv;
-    const int64_t n = slab_rows * width;
-    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-    unsigned char* ws = (unsigned char*)wsv;
-    WT* g = (WT*)ws;
-    double* fbuf = (double*)(ws + up(n * sizeof(WT)));
-    WT* wbuf = (WT*)(ws + up(n * sizeof(WT)) + up(n * sizeof(double)));
-    constexpr int RB = sizeof(WT) == 4 ? POLSAR_NLM_RB : 2;
-    constexpr int NS = POLSAR_NLM_NS;
-    CUtensorMap wmap, wmap2;
-    const int64_t P = slab_rows * weight_pitch<WT>(width);
-    if (!nlm_weight_map2<WT>(&wmap, wbuf, P, fwd_count(R), 1) ||
-        !nlm_weight_map2<WT>(&wmap2, wbuf, P, fwd_count(R), 2 * R + 1))
-        return fail(POLSAR_ECUDA, "polsar_nlm_filter: cuTensorMapEncodeTiled failed");
-    const size_t smem = nlm_smem_bytes<WT>(R, RB, NS, sizeof(S));
-    auto kern = R == 11 ? k_nlm_gather<S, WT, 11, RB, NS> : k_nlm_gather<S, WT, 0, RB, NS>;
-    if (smem > K3_SMEM_MAX ||
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_nlm_filter: shared memory request too large");
-    k_window_prep<S, T, WT><<<grid_for(n, 256), 256, 0, s>>>(z, ld, n, g);
-    const double alpha = looks / (2.0 * h);
-    int rc = alpha == 2.0
-                 ? launch_fwd<LogDetPair<S, T, WT, 1>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
-                       LogDetPair<S, T, WT, 1>{z, ld, g, (WT)alpha, true}, width, slab_rows, rb, re, R,
-                       wbuf, fbuf, s, "polsar_nlm_filter: shared memory request too large")
-                 : launch_fwd<LogDetPair<S, T, WT, 0>, POLSAR_SYM_TY, POLSAR_SYM_RB>(
-                       LogDetPair<S, T, WT, 0>{z, ld, g, (WT)alpha, false}, width, slab_rows, rb, re, R,
-                       wbuf, fbuf, s, "polsar_nlm_filter: shared memory request too large");
-    if (rc != POLSAR_OK) return rc;
-    constexpr int COLS = NLM_TX - 16 / (int)sizeof(WT);
-    dim3 grid((unsigned)((width + COLS - 1) / COLS), (unsigned)((re - rb + RB - 1) / RB));
-    kern<<<grid, NLM_TX, smem, s>>>(wmap, wmap2, z, ld, width, slab_rows, rb, re, R, (S*)out_w, (S*)out_z, ld_out);
-    return launch_check("polsar_nlm_filter: launch failed");
-}
-
-// NLM variant: symmetric (pass 1 + gather, default for R <= V3_RMAX) or the
-// direct form (POLSAR_NLM_VARIANT=direct, and always for R > V3_RMAX).
-bool nlm_direct() {
-    static const bool v = [] {
-        const char* e = getenv("POLSAR_NLM_VARIANT");
-        return e && e[0] == 'd';
-    }();
-    return v;
-}
-
-}  // namespace
-}  // namespace polsar_impl
+//   the window workspace queries (all three entry points, K4 included)
+// Kernels and launchers: window_core.cuh.
+#include "window_core.cuh"
 
 using namespace polsar_impl;
 
@@ -2099,56 +134,6 @@ int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows
             return launch_window_kl<double, double>(z, ld, width, slab_rows, out_row_begin,
                                                     out_row_end, radius, looks, h, workspace, out, s);
         default: return fail(POLSAR_ENOTSUP, "polsar_window_kl: fp32-arithmetic mode not provided");
-    }
-}
-
-int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
-                      int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
-                      double h, void* workspace, void* out_w, void* out_z, int64_t ld_out,
-                      int dtype, void* cuda_stream) {
-    if (width < 0 || slab_rows < 0) return fail(POLSAR_EINVAL, "negative size");
-    if (out_row_begin < 0 || out_row_end < out_row_begin || out_row_end > slab_rows)
-        return fail(POLSAR_EINVAL, "bad output row range");
-    if (radius < 0 || radius > 16) return fail(POLSAR_EINVAL, "radius out of [0, 16]");
-    if (!(looks > 0) || !(h > 0)) return fail(POLSAR_EINVAL, "looks and h must be > 0");
-    if (ld < slab_rows * width) return fail(POLSAR_EINVAL, "ld < slab_rows*width");
-    if (ld_out < (out_row_end - out_row_begin) * width) return fail(POLSAR_EINVAL, "ld_out too small");
-    if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
-    if (!z || !workspace || !out_z) return fail(POLSAR_EINVAL, "null pointer");
-    cudaStream_t s = (cudaStream_t)cuda_stream;
-    // (the symmetric form's gather addresses a weight plane with 32-bit TMA coordinates)
-    if (radius >= 1 && radius <= V3_RMAX && !nlm_direct() && tensor_map_encoder() &&
-        slab_rows * (width + 4) + 2 * NLM_TX < ((int64_t)1 << 31)) {
-        switch (dtype) {
-            case POLSAR_F32:
-                return launch_nlm_sym<float, double, float>(z, ld, width, slab_rows, out_row_begin,
-                                                            out_row_end, radius, looks, h, workspace,
-                                                            out_w, out_z, ld_out, s);
-            case POLSAR_F64:
-            case POLSAR_F64_PLAIN:
-                return launch_nlm_sym<double, double, double>(z, ld, width, slab_rows, out_row_begin,
-                                                              out_row_end, radius, looks, h, workspace,
-                                                              out_w, out_z, ld_out, s);
-            case POLSAR_F32_PLAIN:
-                return launch_nlm_sym<float, float, float>(z, ld, width, slab_rows, out_row_begin,
-                                                           out_row_end, radius, looks, h, workspace,
-                                                           out_w, out_z, ld_out, s);
-            default: return fail(POLSAR_EINVAL, "bad dtype");
-        }
-    }
-    switch (dtype) {
-        case POLSAR_F32:
-            return launch_nlm<float, double, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
-                                                    radius, looks, h, workspace, out_w, out_z, ld_out, s);
-        case POLSAR_F64:
-        case POLSAR_F64_PLAIN:
-            return launch_nlm<double, double, double>(z, ld, width, slab_rows, out_row_begin,
-                                                      out_row_end, radius, looks, h, workspace, out_w,
-                                                      out_z, ld_out, s);
-        case POLSAR_F32_PLAIN:
-            return launch_nlm<float, float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
-                                                   radius, looks, h, workspace, out_w, out_z, ld_out, s);
-        default: return fail(POLSAR_EINVAL, "bad dtype");
     }
 }
 
