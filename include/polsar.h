@@ -115,7 +115,8 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radiu
 
 /* polsar_window_workspace_bytes_for -- the same for one entry point:
  * entry 0 polsar_window_distance, 1 polsar_nlm_filter, 2 polsar_window_kl
- * (0 for an invalid entry or an unsupported dtype / radius).  A workspace of
+ * (0 for an invalid entry, negative or > 2^40-pixel sizes, or an
+ * unsupported dtype / radius).  A workspace of
  * this size serves every call of that entry point with these sizes in this
  * process.  The window and KL sums need ~40 B per pixel, so a UAVSAR-scale
  * slab (4e8 pixels) fits where the NLM's weight planes (~1 KB per pixel)
@@ -129,7 +130,8 @@ size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t w
  *   d_ij = L [ln det((Z_i + Z_j)/2) - (ln det Z_i + ln det Z_j)/2],
  * N(i) the (2R+1)x(2R+1) window centred on i clipped to the image (R-12).
  *   z         : device, 9 planes of a slab of slab_rows x width pixels
- *               (row-major), plane stride ld >= slab_rows*width.  The slab is
+ *               (row-major, slab_rows*width <= 2^40, else EINVAL), plane
+ *               stride ld >= slab_rows*width.  The slab is
  *               exactly the in-image rows around the output rows, so clipping
  *               at the slab edge equals clipping at the image edge.
  *   out_row_begin, out_row_end : slab rows whose W is written (0 <= b <= e

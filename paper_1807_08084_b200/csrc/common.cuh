@@ -36,6 +36,13 @@ namespace polsar_impl {
 int fail(int code, const char* msg);
 int launch_check(const char* what);
 
+// Image extents the window-family entry points accept: slab_rows * width <=
+// 2^40 pixels (far beyond any HBM; keeps every byte count below in int64)
+constexpr int64_t kMaxSlabPixels = (int64_t)1 << 40;
+__host__ __forceinline__ bool slab_size_ok(int64_t slab_rows, int64_t width) {
+    return slab_rows >= 0 && width >= 0 && (width == 0 || slab_rows <= kMaxSlabPixels / width);
+}
+
 // --------------------------------------------------------- launch geometry
 int num_sms();
 // one thread per work item, the whole batch in one grid (capped at 2^31-1

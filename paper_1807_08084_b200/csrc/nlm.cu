@@ -533,7 +533,7 @@ int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_row
                       int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
                       double h, void* workspace, void* out_w, void* out_z, int64_t ld_out,
                       int dtype, void* cuda_stream) {
-    if (width < 0 || slab_rows < 0) return fail(POLSAR_EINVAL, "negative size");
+    if (!slab_size_ok(slab_rows, width)) return fail(POLSAR_EINVAL, "negative size or slab_rows*width > 2^40");
     if (out_row_begin < 0 || out_row_end < out_row_begin || out_row_end > slab_rows)
         return fail(POLSAR_EINVAL, "bad output row range");
     if (radius < 0 || radius > 16) return fail(POLSAR_EINVAL, "radius out of [0, 16]");

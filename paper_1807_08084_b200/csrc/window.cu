@@ -14,7 +14,7 @@ extern "C" {
 
 size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t width, int radius,
                                          int dtype) {
-    if (slab_rows < 0 || width < 0 || radius < 0 || entry < 0 || entry > 2) return 0;
+    if (!slab_size_ok(slab_rows, width) || radius < 0 || entry < 0 || entry > 2) return 0;
     const int64_t n = slab_rows * width;
     const bool wt64 = dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN;
     const size_t wt = wt64 ? 8 : 4;
@@ -64,7 +64,7 @@ size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radiu
 int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
                            int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
                            double h, void* workspace, void* out, int dtype, void* cuda_stream) {
-    if (width < 0 || slab_rows < 0) return fail(POLSAR_EINVAL, "negative size");
+    if (!slab_size_ok(slab_rows, width)) return fail(POLSAR_EINVAL, "negative size or slab_rows*width > 2^40");
     if (out_row_begin < 0 || out_row_end < out_row_begin || out_row_end > slab_rows)
         return fail(POLSAR_EINVAL, "bad output row range");
     if (radius < 0 || radius > 16) return fail(POLSAR_EINVAL, "radius out of [0, 16]");
@@ -109,7 +109,7 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
 int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows,
                      int64_t out_row_begin, int64_t out_row_end, int radius, double looks,
                      double h, void* workspace, void* out, int dtype, void* cuda_stream) {
-    if (width < 0 || slab_rows < 0) return fail(POLSAR_EINVAL, "negative size");
+    if (!slab_size_ok(slab_rows, width)) return fail(POLSAR_EINVAL, "negative size or slab_rows*width > 2^40");
     if (out_row_begin < 0 || out_row_end < out_row_begin || out_row_end > slab_rows)
         return fail(POLSAR_EINVAL, "bad output row range");
     if (radius < 0 || radius > V3_RMAX) return fail(POLSAR_EINVAL, "radius out of [0, 12]");

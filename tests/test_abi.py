@@ -64,6 +64,13 @@ def test_loads_and_validates_without_gpu():
     assert lib.polsar_window_distance(None, 0, 4, 4, 0, 5, 11, 4.0, 1.0, None, None, 0, None) == 1
     assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 17, 4.0, 1.0, None, None, 0, None) == 1
     assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 3, 0.0, 1.0, None, None, 0, None) == 1
+    big = 1 << 31  # slab_rows * width = 2^62 > 2^40: refused before any size arithmetic
+    assert lib.polsar_window_distance(None, 1 << 62, big, big, 0, 1, 11, 4.0, 1.0, None, None, 0, None) == 1
+    assert b"2^40" in lib.polsar_last_error()
+    assert lib.polsar_window_kl(None, 1 << 62, big, big, 0, 1, 11, 4.0, 1.0, None, None, 0, None) == 1
+    assert lib.polsar_nlm_filter(None, 1 << 62, big, big, 0, 1, 11, 4.0, 1.0, None, None, None, 1 << 31,
+                                 0, None) == 1
+    assert lib.polsar_window_workspace_bytes(big, big, 11, 0) == 0
     assert lib.polsar_checksum(None, 5, 2, 1, 0, 0, None, None, None) == 1
     assert lib.polsar_inv_det_host(None, None, None, 5, 5, 0, 0, None, 0, None, None, None) == 1
     assert lib.polsar_window_workspace_bytes(2048, 2048, 11, 0) >= 2048 * 2048 * (4 + 8 + 264 * 4)
