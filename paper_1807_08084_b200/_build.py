@@ -23,7 +23,8 @@ TARGETS = {
         out=os.path.join(PKG, "libpolsar.so"),
         srcs=[os.path.join(PKG, "csrc", f) for f in ("abi.cu", "inv_det.cu", "window.cu", "nlm.cu", "checksum.cu")],
         deps=[os.path.join(INCLUDE, "polsar.h"), os.path.join(PKG, "csrc", "common.cuh"),
-              os.path.join(PKG, "csrc", "alg.cuh"), os.path.join(PKG, "csrc", "window_core.cuh")],
+              os.path.join(PKG, "csrc", "alg.cuh"), os.path.join(PKG, "csrc", "window_core.cuh"),
+              os.path.join(PKG, "csrc", "window_mma.cuh")],
         cmd=lambda out, srcs: [NVCC] + NVCC_COMMON + srcs + ["-o", out],
     ),
     # seeded input generator, GPU build (support; FMA contraction off so it

@@ -1,0 +1,334 @@
+// window_mma.cuh -- part of libpolsar.so (B200, sm_100a); arXiv 1807.08084.
+// K3b pass 1 on the FP64 tensor cores (A/B variant, POLSAR_WINDOW_MMA=1).
+//
+// The pair determinant of the log-det window (BASELINE
+// configs[4]) through the 3x3 identity
+//   det(A + B) = det A + det B + <adj A, B> + <A, adj B>,   <X, Y> = tr(X Y),
+// (the expansion form of K3 v3) is the dot product of two
+// 20-vectors,
+//   a_i = [adj2(Z_i), Z_i, D_i, 1],   b_j = [Z_j, adj2(Z_j), 1, D_j],
+// adj2 = the adjugate of Eq. 3 with its off-diagonal entries doubled (the
+// Hermitian inner product counts each off-diagonal pair twice), D = det by
+// Eq. 6.  So an 8 x 8 block of pair determinants (8 owned pixels of a row x 8
+// window pixels of a row) is one 8 x 8 x 20 fp64 matrix product: five
+// mma.sync.m8n8k4.f64 (DMMA).  Each warp keeps the a-fragments of its
+// 2 rows x 8 pixels in registers (5 doubles per row per lane) and streams the
+// b-fragments of the window rows from shared memory.  The symmetric two-pass
+// structure of the ACC form (window_core.cuh) is kept: pass 1 covers the
+// forward half-window (dy = 1..R, and dy = 0 with dx = 1..R) and adds every
+// weight to the neighbour's fixed-point backward sum in shared memory; pass 2
+// is k_window_bwd_acc unchanged (tile height 8).
+//
+// Per 8-pixel group and window row the 8 + 2R window columns are covered by
+// NT = ceil((8 + 2R) / 8) column blocks of 8 (72 % of the computed pairs are
+// inside the window at R = 11): 47 blocks x 5 DMMA x 256 FMA per 8 pixels, an
+// FP64 floor of 1.69 ms at c5, the same as the scalar form's 29 operations per
+// pair (1.72 ms) -- the gain sought is the tensor pipe's issue efficiency
+// (62.6 of 64 FMA/clk/SM at 16 warps, profiles/r01_micro_dmma_rate.txt)
+// against the scalar pair loop's 57 %.
+#pragma once
+#include "window_core.cuh"
+
+namespace polsar_impl {
+namespace {
+
+#ifndef POLSAR_MMA_TY
+#define POLSAR_MMA_TY 8
+#endif
+constexpr int MMA_TY = POLSAR_MMA_TY;  // tile rows (pass 2 takes the same TY)
+constexpr int MMA_RB = 2;              // owned rows per warp
+constexpr int MMA_THREADS = 32 * (K3_TX / 8) * (MMA_TY / MMA_RB);  // one warp per 8 x RB pixels
+constexpr int MMA_RS = 20;             // record doubles: Z (9) | adj2 (9) | 1 | D  (160 B:
+                                       // a warp's b-fragment loads hit 32 distinct banks per half)
+
+bool window_mma() {
+    static const bool v = [] {
+        const char* e = getenv("POLSAR_WINDOW_MMA");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+__host__ __device__ constexpr int mma_nt(int R) { return (2 * R + 15) / 8; }
+// halo columns: x0 - R .. x0 - R + HWe - 1 (the last group's NT blocks may
+// reach 2 columns past the window; those pairs are masked)
+__host__ __device__ constexpr int mma_hwe(int R) { return K3_TX - 8 + 8 * mma_nt(R); }
+
+template <typename WT>
+size_t mma_fwd_smem(int R) {
+    const size_t slots = (size_t)mma_hwe(R) * (MMA_TY + R);
+    return slots * (MMA_RS * sizeof(double) + sizeof(WT) + 2 * sizeof(unsigned));
+}
+
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+}
+
+// One halo record from the 9 planes: Z, the doubled adjugate (Eq. 3), 1, D
+// (Eq. 6, the same det_eq6 as k_window_prep, so g is bit-identical to it).
+template <typename S, typename WT>
+__device__ __forceinline__ void mma_fill(double* rec, WT* gs, const S* __restrict__ z, int64_t ld, int64_t p,
+                                         bool in) {
+    double v[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = in ? (double)z[k * ld + p] : 0.0;
+    const double a = v[0], br = v[1], bi = v[2], cr = v[3], ci = v[4], d = v[5], er = v[6], ei = v[7],
+                 f = v[8];
+    const double A00 = FMA(d, f, -FMA(er, er, MUL(ei, ei)));
+    const double A01r = FMA(cr, er, FMA(ci, ei, -MUL(br, f)));   // c conj(e) - b f
+    const double A01i = FMA(ci, er, -FMA(cr, ei, MUL(bi, f)));
+    const double A02r = FMA(br, er, -FMA(bi, ei, MUL(cr, d)));   // b e - c d
+    const double A02i = FMA(br, ei, FMA(bi, er, -MUL(ci, d)));
+    const double A11 = FMA(a, f, -FMA(cr, cr, MUL(ci, ci)));
+    const double A12r = FMA(br, cr, FMA(bi, ci, -MUL(a, er)));   // conj(b) c - a e
+    const double A12i = FMA(br, ci, -FMA(bi, cr, MUL(a, ei)));
+    const double A22 = FMA(a, d, -FMA(br, br, MUL(bi, bi)));
+    const double D = det_eq6<double>(a, br, bi, cr, ci, d, er, ei, f);
+    const double r[MMA_RS] = {a,    br,         bi,         cr,         ci,         d,   er,
+                              ei,   f,          A00,        2.0 * A01r, 2.0 * A01i, 2.0 * A02r, 2.0 * A02i,
+                              A11,  2.0 * A12r, 2.0 * A12i, A22,        1.0,        D};
+    double2* o = reinterpret_cast<double2*>(rec);
+#pragma unroll
+    for (int k = 0; k < MMA_RS / 2; ++k) o[k] = make_double2(r[2 * k], r[2 * k + 1]);
+    // g = 1 / (8 D) as k_window_prep (NaN marks a pixel that is not positive
+    // definite; 0 an out-of-image slot, never a valid pair)
+    const WT gv = (WT)(1.0 / MUL(8.0, D));
+    *gs = in ? ((D > 0.0 && gv < WT(INFINITY)) ? gv : WT(NAN)) : WT(0);
+}
+
+// the owned operand's k -> record slot: [adj2, Z, D, 1] against the window
+// pixel's record [Z, adj2, 1, D]
+__device__ __forceinline__ int mma_perm(int k) { return k < 9 ? k + 9 : k < 18 ? k - 9 : (k == 18 ? 19 : 18); }
+
+// Fragment roles: the window pixels are the MMA's A operand (rows m, streamed
+// from shared memory per 8-pixel block) and the owned pixels its B operand
+// (columns n, register-resident), so lane (m = lane/4, q = lane%4) holds the
+// pairs (window pixel m, owned pixels 2q and 2q+1).  A window pixel's
+// backward sum then needs a reduction over only the 4 lanes of its row, and
+// the forward sums are reduced once, at the end of the kernel.
+template <typename WT>
+struct MmaLane {
+    int am, kq, b0;         // fragment row / k, first C column
+    unsigned mfull, mzero;  // window-and-image masks over (block t, column e): dy > 0, dy == 0
+};
+
+// One window row (slot jrow = its first block's first pixel) against the
+// warp's RB owned rows: per 8-pixel block, the A fragment, RB chains of 5
+// DMMA, the weights into rp (forward) and the row's fixed-point sums into
+// the backward counters.  FULL: dy = wy - r in [1, R] for every r (no
+// branches, so the scheduler interleaves the chains).
+template <typename WT, bool A2, int NT, bool FULL>
+__device__ __forceinline__ void mma_row(const double* rec, const WT* gs, unsigned* ah, int HPe, int jrow,
+                                        const double (&bo)[MMA_RB][5], const WT (&gi)[MMA_RB][2],
+                                        const bool (&own)[MMA_RB][2], int wy, int R, WT alpha,
+                                        const MmaLane<WT>& ln, WT (&rp)[MMA_RB][2]) {
+#pragma unroll
+    for (int r = 0; r < MMA_RB; ++r) rp[r][0] = rp[r][1] = WT(0);
+    long long vs[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const int jb = jrow + 8 * t;  // slot of the block's first window pixel
+        const double* ra = rec + (size_t)MMA_RS * (jb + ln.am) + ln.kq;
+        double aw[5];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) aw[s] = ra[4 * s];
+        const WT gj = gs[jb + ln.am];
+        long long v = 0ll;
+#pragma unroll
+        for (int r = 0; r < MMA_RB; ++r) {
+            const int dy = wy - r;
+            if (!FULL && (dy < 0 || dy > R)) continue;  // warp-uniform
+            double c[2] = {0.0, 0.0};
+#pragma unroll
+            for (int s = 0; s < 5; ++s) dmma_884(c, aw[s], bo[r][s]);
+            const unsigned m = (FULL || dy > 0) ? ln.mfull : ln.mzero;
+            WT wb = WT(0);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const WT fds = (WT)c[e];
+                const WT rr = (fds * gj) * (fds * gi[r][e]);
+                WT w = pair_weight(rr, alpha, A2);
+                w = ((m >> (2 * t + e)) & 1u) ? w : WT(0);
+                rp[r][e] += w;
+                wb += own[r][e] ? w : WT(0);
+            }
+            // the two owned columns 2q, 2q+1 are fixed by x mod 8, so this
+            // float sum is the same under any row decomposition; the rest is
+            // integer (exact, order-free)
+            v += fixed_w(wb);
+        }
+        // sum over the 4 lanes of the window pixel's fragment row
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        vs[t] = v;
+    }
+    // one shared-memory add per window pixel, after all blocks (a branch per
+    // block would split the row into basic blocks the scheduler cannot overlap)
+    if (ln.kq == 0) {
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc_add(ah, HPe, jrow + 8 * t + ln.am, vs[t]);
+    }
+}
+
+template <typename S, typename WT, bool A2, int NT>
+__global__ void __launch_bounds__(MMA_THREADS, 1)
+k_window_fwd_mma(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows, int64_t row_begin,
+                 int64_t row_end, int R, WT alpha, double* __restrict__ fbuf, long long* __restrict__ part) {
+    constexpr int TY = MMA_TY, RB = MMA_RB;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int HWe = K3_TX - 8 + 8 * NT;
+    const int HH = TY + R;
+    const int HPe = HWe * HH;
+    double* rec = reinterpret_cast<double*>(smem_raw);
+    WT* gs = reinterpret_cast<WT*>(rec + (size_t)MMA_RS * HPe);
+    unsigned* ah = reinterpret_cast<unsigned*>(gs + HPe);  // high counters, then low
+
+    const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
+    const int64_t y0 = row_begin + (int64_t)blockIdx.y * TY;
+    for (int q = threadIdx.x; q < HPe; q += blockDim.x) {
+        const int hy = q / HWe, hx = q % HWe;
+        const int64_t gy = y0 + hy, gx = x0 - R + hx;
+        const bool in = gy < slab_rows && gx >= 0 && gx < width;
+        mma_fill<S, WT>(rec + (size_t)MMA_RS * q, gs + q, z, ld, in ? gy * width + gx : 0, in);
+        ah[q] = 0u;
+        ah[HPe + q] = 0u;
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cg = warp % (K3_TX / 8), rg = warp / (K3_TX / 8);
+    const int am = lane >> 2;  // A row (window pixel of a block) / B column (owned pixel of the B fragment)
+    const int kq = lane & 3;   // fragment k / C column pair
+    const int b0 = 2 * kq;     // this lane's C columns: owned pixels b0, b0 + 1
+
+    double bo[RB][5];
+    WT gi[RB][2];
+    bool own[RB][2];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        const int hr = (rg * RB + r) * HWe + R + 8 * cg;  // slot of the group's first owned pixel
+        const int64_t gy = y0 + rg * RB + r;
+#pragma unroll
+        for (int s = 0; s < 5; ++s) bo[r][s] = rec[(size_t)MMA_RS * (hr + am) + mma_perm(4 * s + kq)];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            gi[r][e] = gs[hr + b0 + e];
+            own[r][e] = x0 + 8 * cg + b0 + e < width && gy < row_end;
+        }
+        // rare: flag an invalid owned pixel and its forward targets (R-19)
+        const bool bad = x0 + 8 * cg + am < width && gy < row_end && !(gs[hr + am] > WT(0));
+        if (bad && kq == 0) {
+            const int qa = hr + am;
+            atomicOr(ah + HPe + qa, kBadBit);
+            for (int dy = 0; dy <= R; ++dy)
+                for (int dx = (dy == 0 ? 1 : -R); dx <= R; ++dx) atomicOr(ah + HPe + qa + dy * HWe + dx, kBadBit);
+        }
+    }
+    // per-lane masks over (t, e): the window column test for dy > 0 and dy == 0,
+    // and the image column test of the window pixel
+    unsigned mfull = 0u, mzero = 0u;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const int64_t gxj = x0 + 8 * cg - R + 8 * t + am;
+        const bool col = gxj >= 0 && gxj < width;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int dx = 8 * t + am - b0 - e - R;  // window pixel column - owned pixel column
+            mfull |= (unsigned)(col && dx >= -R && dx <= R) << (2 * t + e);
+            mzero |= (unsigned)(col && dx >= 1 && dx <= R) << (2 * t + e);
+        }
+    }
+
+    double acc[RB][2];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r][0] = acc[r][1] = 0.0;
+    const MmaLane<WT> ln{am, kq, b0, mfull, mzero};
+    for (int wy = 0; wy <= R + RB - 1; ++wy) {
+        const int hy = rg * RB + wy;
+        if (y0 + hy >= slab_rows) break;  // warp-uniform
+        WT rp[RB][2];
+        const int jrow = hy * HWe + 8 * cg;
+        if (wy >= RB && wy <= R)  // every owned row sees this row at dy in [1, R]: no branches
+            mma_row<WT, A2, NT, true>(rec, gs, ah, HPe, jrow, bo, gi, own, wy, R, alpha, ln, rp);
+        else
+            mma_row<WT, A2, NT, false>(rec, gs, ah, HPe, jrow, bo, gi, own, wy, R, alpha, ln, rp);
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) acc[r][e] += (double)rp[r][e];
+    }
+    // forward sums: the 8 lanes of a C column hold disjoint window pixels
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double a = acc[r][e];
+            a += __shfl_xor_sync(0xffffffffu, a, 4);
+            a += __shfl_xor_sync(0xffffffffu, a, 8);
+            a += __shfl_xor_sync(0xffffffffu, a, 16);
+            if (am == 0 && own[r][e]) fbuf[(y0 + rg * RB + r) * width + x0 + 8 * cg + b0 + e] = a;
+        }
+    __syncthreads();
+    // the tile's halo-region sums in pass 2's layout (HW = K3_TX + 2R columns)
+    const int HW = K3_TX + 2 * R;
+    const int HP = HW * HH;
+    long long* dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * HP;
+    for (int q = threadIdx.x; q < HP; q += blockDim.x) {
+        const int sq = (q / HW) * HWe + q % HW;
+        const unsigned lo = ah[HPe + sq];
+        dst[q] = (lo & kBadBit) ? kBadSum : (long long)(((unsigned long long)ah[sq] << 22) + lo);
+    }
+}
+
+// workspace: F (N doubles) | the tiles' backward sums (pass-1 grid of tile height MMA_TY)
+inline size_t mma_sym_bytes(int64_t slab_rows, int64_t width, int R) {
+    return acc_sym_bytes(0, slab_rows, width, R, MMA_TY);
+}
+
+template <typename S, typename WT, bool A2, int NT>
+int launch_fwd_mma(const S* z, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re, int R,
+                   WT alpha, double* fbuf, long long* part, cudaStream_t s) {
+    const FwdGrid fg = fwd_grid(width, rb, re, R, MMA_TY);
+    const size_t smem = mma_fwd_smem<WT>(R);
+    auto kern = k_window_fwd_mma<S, WT, A2, NT>;
+    if (smem > K3_SMEM_MAX ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
+    dim3 grid((unsigned)fg.nbx, (unsigned)fg.nby);
+    kern<<<grid, MMA_THREADS, smem, s>>>(z, ld, width, slab_rows, fg.p0, re, R, alpha, fbuf, part);
+    return POLSAR_OK;
+}
+
+template <typename S, typename WT, bool A2>
+int launch_fwd_mma_r(const S* z, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re, int R,
+                     WT alpha, double* fbuf, long long* part, cudaStream_t s) {
+    switch (mma_nt(R)) {
+        case 1: return launch_fwd_mma<S, WT, A2, 1>(z, ld, width, slab_rows, rb, re, R, alpha, fbuf, part, s);
+        case 2: return launch_fwd_mma<S, WT, A2, 2>(z, ld, width, slab_rows, rb, re, R, alpha, fbuf, part, s);
+        case 3: return launch_fwd_mma<S, WT, A2, 3>(z, ld, width, slab_rows, rb, re, R, alpha, fbuf, part, s);
+        default: return launch_fwd_mma<S, WT, A2, 4>(z, ld, width, slab_rows, rb, re, R, alpha, fbuf, part, s);
+    }
+}
+
+// The log-det window, tensor-core pass 1 + pass 2 (R <= V3_RMAX).
+template <typename S, typename WT>
+int launch_window_mma(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re,
+                      int R, double looks, double h, void* wsv, void* outv, cudaStream_t s) {
+    const S* z = (const S*)zv;
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    unsigned char* ws = (unsigned char*)wsv;
+    double* fbuf = (double*)ws;
+    long long* part = (long long*)(ws + up((size_t)slab_rows * width * sizeof(double)));
+    const double alpha = looks / (2.0 * h);
+    const int rc = alpha == 2.0
+                       ? launch_fwd_mma_r<S, WT, true>(z, ld, width, slab_rows, rb, re, R, (WT)alpha, fbuf, part, s)
+                       : launch_fwd_mma_r<S, WT, false>(z, ld, width, slab_rows, rb, re, R, (WT)alpha, fbuf, part, s);
+    if (rc != POLSAR_OK) return rc;
+    launch_bwd_acc<S>(part, fbuf, width, rb, re, R, MMA_TY, outv, s);
+    return launch_check("polsar_window_distance: launch failed");
+}
+
+}  // namespace
+}  // namespace polsar_impl
