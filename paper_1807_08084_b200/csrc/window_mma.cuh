@@ -241,9 +241,12 @@ k_window_fwd_mma(const S* __restrict__ z, int64_t ld, int64_t width, int64_t sla
         }
     }
 
-    double acc[RB][2];
+    // forward sums as fixed-point integers too (each row's float sum rounded
+    // to 2^-44): integer adds keep them off the FP64 pipe the DMMAs use
+    long long acc[RB][2];
+    unsigned fnan = 0u;  // (r, e) bits: a NaN weight entered that forward sum (R-19)
 #pragma unroll
-    for (int r = 0; r < RB; ++r) acc[r][0] = acc[r][1] = 0.0;
+    for (int r = 0; r < RB; ++r) acc[r][0] = acc[r][1] = 0ll;
     const MmaLane<WT> ln{am, kq, b0, mfull, mzero};
     for (int wy = 0; wy <= R + RB - 1; ++wy) {
         const int hy = rg * RB + wy;
@@ -257,18 +260,25 @@ k_window_fwd_mma(const S* __restrict__ z, int64_t ld, int64_t width, int64_t sla
 #pragma unroll
         for (int r = 0; r < RB; ++r)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) acc[r][e] += (double)rp[r][e];
+            for (int e = 0; e < 2; ++e) {
+                acc[r][e] += fixed_w(rp[r][e]);
+                fnan |= (unsigned)(rp[r][e] != rp[r][e]) << (2 * r + e);
+            }
     }
     // forward sums: the 8 lanes of a C column hold disjoint window pixels
 #pragma unroll
     for (int r = 0; r < RB; ++r)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            double a = acc[r][e];
+            long long a = acc[r][e];
             a += __shfl_xor_sync(0xffffffffu, a, 4);
             a += __shfl_xor_sync(0xffffffffu, a, 8);
             a += __shfl_xor_sync(0xffffffffu, a, 16);
-            if (am == 0 && own[r][e]) fbuf[(y0 + rg * RB + r) * width + x0 + 8 * cg + b0 + e] = a;
+            const unsigned nanl = __ballot_sync(0xffffffffu, (fnan >> (2 * r + e)) & 1u);
+            const bool isnan_f = (nanl & (0x11111111u << kq)) != 0u;
+            if (am == 0 && own[r][e])
+                fbuf[(y0 + rg * RB + r) * width + x0 + 8 * cg + b0 + e] =
+                    isnan_f ? __longlong_as_double(0x7ff8000000000000ll) : (double)a * (1.0 / (double)kFix);
         }
     __syncthreads();
     // the tile's halo-region sums in pass 2's layout (HW = K3_TX + 2R columns)
