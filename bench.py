@@ -507,7 +507,9 @@ def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
             plain=plain, stream=stream), steps)
         res[f"window_c5{'_plain' if plain else ''}"] = {
             "pairs_per_s": pairs / t, "ms": t * 1e3, "pairs": pairs,
-            "mode": "fp32 storage, fp32 weight, " + ("fp32 pair det" if plain else "fp64 pair det")}
+            "mode": "fp32 storage, fp32 weight, " + ("fp32 pair det" if plain else "fp64 pair det") +
+                    ("" if plain or os.environ.get("POLSAR_WINDOW_MMA", "") == "0"
+                     else " (DMMA mixed-discriminant pass 1)")}
     # K6 (KL window) and K4 (NLM filter) on the same c5 input
     t = _time_kernel(torch, stream, lambda: P.polsar_window_kl(
         z5, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, w5, stream=stream), steps)
@@ -575,7 +577,7 @@ def verify_sample(P, z, out, status, cfg, r0):
 
 # FP64 pipe peak: 64 lanes / clk / SM x 148 SMs x 1.965 GHz
 FP64_PEAK_OPS = 64 * 148 * 1.965e9
-FP64_OPS_PER_PAIR = {"window": 29, "nlm": 40, "kl": 19}
+FP64_OPS_PER_PAIR = {"window": 29, "window_mma": 20, "nlm": 40, "kl": 19}
 
 
 def run_window(args):
@@ -655,6 +657,7 @@ def run_window(args):
     pairs = pairs_rank * world
     ops = FP64_OPS_PER_PAIR[args.kernel]
     # which form the library runs (read once per process, as the library does)
+    mma = False
     if args.kernel == "nlm":
         symmetric = not os.environ.get("POLSAR_NLM_VARIANT", "").startswith("d") and R <= 12
         variant = "symmetric two-pass (pass 1 + TMA gather)" if symmetric else "direct"
@@ -664,13 +667,21 @@ def run_window(args):
         variant = "symmetric two-pass" if symmetric else {"3": "det expansion", "2": "direct"}.get(v, v)
         if args.kernel == "kl" and not symmetric:
             variant = "streaming expansion"
+        # the tensor-core pass 1 (csrc/window_mma.cuh; default for the fp32-storage log-det
+        # window): each unordered pair is a 20-term fp64 dot product, 20 FMAs on the same
+        # FP64 datapath (DMMA.8x8x4 shares the 64 FMA/clk/SM peak)
+        mma = (args.kernel == "window" and symmetric and os.environ.get("POLSAR_WINDOW_MMA", "") != "0"
+               and os.environ.get("POLSAR_WINDOW_PLANES", "") != "1" and cfg.dtype == "float32")
+        if mma:
+            variant = "symmetric two-pass, pass 1 on the FP64 tensor cores (DMMA)"
+            ops = FP64_OPS_PER_PAIR["window_mma"]
     if symmetric:
         # d(i, j) is symmetric: the algorithmic FP64 work is one evaluation per
         # unordered pair, which is what the symmetric kernels do;
         # NLM's gather pass adds no FP64 work (9 FP32 FMAs per ordered pair)
         work_pairs = unordered_pairs_rows(H, W, R, r0, r1)
-        ops = FP64_OPS_PER_PAIR["window"] if args.kernel == "nlm" else ops
-        launches = 3  # prep, forward pass, backward / gather pass
+        ops = FP64_OPS_PER_PAIR["window"] if args.kernel == "nlm" else ops  # (NLM's pass 1 is scalar)
+        launches = 2 if mma else 3  # (prep,) forward pass, backward / gather pass
     else:
         work_pairs = pairs_rank
         launches = 2  # prep, window sum
@@ -688,6 +699,9 @@ def run_window(args):
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": FP64_PEAK_OPS / 1e12,
                      "unit": "T fp64-ops/s", "frac": achieved / FP64_PEAK_OPS, "traffic": None,
                      "ops_per_pair": ops, "pairs_evaluated": work_pairs,
+                     **({"issued_fma_per_pair": mma_issued_per_pair(R),
+                         "issued_frac": mma_issued_per_pair(R) * work_pairs / (t_local / steps) / FP64_PEAK_OPS}
+                        if mma else {}),
                      "timed": "whole call (prep + all passes), CUDA events on the launch stream",
                      "peak_source": "64 FP64 lanes/clk/SM x 148 SMs x 1.965 GHz (DESIGN.md §6)"},
         "clocks": sampler.summary(), "gpu_launches": launches * steps,
@@ -708,6 +722,14 @@ def window_pairs_rows(h, w, r, r0, r1):
     xs = np.arange(w)
     nx = np.minimum(w - 1, xs + r) - np.maximum(0, xs - r) + 1
     return int(ny.sum()) * int(nx.sum())
+
+
+def mma_issued_per_pair(r):
+    """DMMA FMAs the tensor-core pass 1 issues per unordered pair of an interior
+    pixel: (R+1) window rows x NT 8-pixel blocks x 5 DMMA x 256 FMA per 8 owned
+    pixels, over the 2R(R+1) pairs each pixel owns (masked pairs included)."""
+    nt = (2 * r + 15) // 8
+    return (r + 1) * nt * 5 * 256 / 8 / (2 * r * (r + 1))
 
 
 def unordered_pairs_rows(h, w, r, r0, r1):

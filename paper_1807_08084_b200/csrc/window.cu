@@ -27,7 +27,7 @@ size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t w
     size_t b = up((size_t)n * wt);  // direct forms: one plane of g
     if (entry == 0) {                // polsar_window_distance
         if (sym_ok && v == 3 && dtype != POLSAR_F32_PLAIN) b = std::max(b, up((size_t)n * 160));
-        if (sym_ok && window_mma() && dtype != POLSAR_F32_PLAIN)
+        if (use_window_mma(dtype, radius))
             b = std::max(b, mma_sym_bytes(slab_rows, width, radius));
         if (sym_ok && v == 4) {
             b = std::max(b, acc_sym_bytes((size_t)n * wt, slab_rows, width, radius, POLSAR_SYM_TY));
@@ -76,7 +76,7 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
     if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
     if (!z || !workspace || !out) return fail(POLSAR_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    if (radius <= V3_RMAX && window_mma() && (dtype == POLSAR_F32 || dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN))
+    if (use_window_mma(dtype, radius))
         return dtype == POLSAR_F32
                    ? launch_window_mma<float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end, radius,
                                                      looks, h, workspace, out, s)

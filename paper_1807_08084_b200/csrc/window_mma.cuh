@@ -1,5 +1,5 @@
 // window_mma.cuh -- part of libpolsar.so (B200, sm_100a); arXiv 1807.08084.
-// K3b pass 1 on the FP64 tensor cores (A/B variant, POLSAR_WINDOW_MMA=1).
+// K3b pass 1 on the FP64 tensor cores (default for fp32 storage; POLSAR_WINDOW_MMA).
 //
 // The pair determinant of the log-det window (BASELINE
 // configs[4]) through the 3x3 identity
@@ -41,12 +41,26 @@ constexpr int MMA_THREADS = 32 * (K3_TX / 8) * (MMA_TY / MMA_RB);  // one warp p
 constexpr int MMA_RS = 20;             // record doubles: Z (9) | adj2 (9) | 1 | D  (160 B:
                                        // a warp's b-fragment loads hit 32 distinct banks per half)
 
-bool window_mma() {
-    static const bool v = [] {
+// POLSAR_WINDOW_MMA: unset = the tensor-core pass 1 for fp32 storage (the
+// default: fp64 storage keeps the scalar pass 1, whose fp64 weights would
+// share the FP64 pipe with the DMMAs); 1 = for both storage precisions; 0 = never.
+int window_mma_mode() {
+    static const int v = [] {
         const char* e = getenv("POLSAR_WINDOW_MMA");
-        return e && e[0] == '1';
+        return e ? (e[0] == '1' ? 1 : e[0] == '0' ? 0 : -1) : -1;
     }();
     return v;
+}
+
+// Does polsar_window_distance run the tensor-core form for this call?  (The
+// workspace query asks the same question.)  The other A/B forms
+// (POLSAR_WINDOW_VARIANT=2/3, POLSAR_WINDOW_PLANES=1) take precedence.
+bool use_window_mma(int dtype, int radius) {
+    if (radius > V3_RMAX || window_variant() != 4 || window_planes()) return false;
+    const int m = window_mma_mode();
+    if (m == 0) return false;
+    if (dtype == POLSAR_F32) return true;
+    return m == 1 && (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN);
 }
 
 __host__ __device__ constexpr int mma_nt(int R) { return (2 * R + 15) / 8; }

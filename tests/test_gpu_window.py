@@ -94,14 +94,21 @@ def test_window_c5_sampled(cuda):
     assert np.all(np.isfinite(got)) and got.min() >= 1 - 1e-6 and got.max() <= 529 + 1e-3
 
 
-@pytest.mark.parametrize("variant", ["2", "3", "planes"])
+VARIANT_ENV = {"2": {"POLSAR_WINDOW_VARIANT": "2"}, "3": {"POLSAR_WINDOW_VARIANT": "3"},
+               "planes": {"POLSAR_WINDOW_PLANES": "1"}, "scalar": {"POLSAR_WINDOW_MMA": "0"},
+               "mma_all": {"POLSAR_WINDOW_MMA": "1"}}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANT_ENV))
 def test_window_variant_subprocess(cuda, variant):
     """The alternative kernels (POLSAR_WINDOW_VARIANT=2: the direct form over
     ordered pairs; 3: the expansion form; POLSAR_WINDOW_PLANES=1: the
     symmetric form through the weight planes instead of the shared-memory
-    backward sums; read once per process) against the oracle in a child
-    process: the log-det window sum, and the KL window sum (variants 2 and 3
-    run KL on the streaming expansion kernel)."""
+    backward sums; POLSAR_WINDOW_MMA=0: the scalar pass 1 for fp32 storage
+    too; =1: the tensor-core pass 1 for fp64 storage too; read once per
+    process) against the oracle in a child process: the log-det window sum,
+    and the KL window sum (variants 2 and 3 run KL on the streaming expansion
+    kernel)."""
     import os
     import subprocess
     import sys
@@ -123,8 +130,7 @@ for dt, tol, tol_kl in ((torch.float32, 2e-5, 2e-5), (torch.float64, 4e-10, 2e-9
     assert e <= tol_kl, ("kl", dt, e)
 print("ok")
 '''
-    env = dict(os.environ, **({"POLSAR_WINDOW_PLANES": "1"} if variant == "planes"
-                              else {"POLSAR_WINDOW_VARIANT": variant}))
+    env = dict(os.environ, **VARIANT_ENV[variant])
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=300)
