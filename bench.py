@@ -514,7 +514,9 @@ def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
     t = _time_kernel(torch, stream, lambda: P.polsar_window_kl(
         z5, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, w5, stream=stream), steps)
     res["kl_window_c5"] = {"pairs_per_s": pairs / t, "ms": t * 1e3, "pairs": pairs,
-                           "mode": "symmetric Wishart KL, fp32 storage, fp64 trace products"}
+                           "mode": "symmetric Wishart KL, fp32 storage, fp64 trace products" +
+                                   ("" if os.environ.get("POLSAR_WINDOW_MMA", "") == "0"
+                                    else " (DMMA pass 1)")}
     zn = torch.empty((9, c5.n), dtype=z5.dtype, device=dev)
     t = _time_kernel(torch, stream, lambda: P.polsar_nlm_filter(
         z5, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, zn, w5, stream=stream), steps)
@@ -670,7 +672,8 @@ def run_window(args):
         # the tensor-core pass 1 (csrc/window_mma.cuh; default for the fp32-storage log-det
         # window): each unordered pair is a 20-term fp64 dot product, 20 FMAs on the same
         # FP64 datapath (DMMA.8x8x4 shares the 64 FMA/clk/SM peak)
-        mma = (args.kernel == "window" and symmetric and os.environ.get("POLSAR_WINDOW_MMA", "") != "0"
+        # (the KL window's too: its two trace products and the -6 are the same 20-term product)
+        mma = (symmetric and os.environ.get("POLSAR_WINDOW_MMA", "") != "0"
                and os.environ.get("POLSAR_WINDOW_PLANES", "") != "1" and cfg.dtype == "float32")
         if mma:
             variant = "symmetric two-pass, pass 1 on the FP64 tensor cores (DMMA)"

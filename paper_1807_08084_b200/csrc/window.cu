@@ -41,6 +41,8 @@ size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t w
                                  : window_sym_bytes<float>(slab_rows, width, radius));
     } else {                         // polsar_window_kl (radius <= 12; no fp32-arithmetic mode)
         if (dtype == POLSAR_F32_PLAIN || !sym_ok) return 0;
+        if (use_window_mma(dtype, radius))  // the tensor-core form: F | tile sums only
+            return std::max(b, mma_sym_bytes(slab_rows, width, radius));
         b = std::max(b, up((size_t)n * 160));  // prepass planes (the streaming form's too)
         if (v == 4) {  // the choice of launch_window_kl_sym
             const size_t pre = (size_t)n * V3_NP * sizeof(double);
@@ -127,6 +129,12 @@ int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows
     if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
     if (!z || !workspace || !out) return fail(POLSAR_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)cuda_stream;
+    if (use_window_mma(dtype, radius))
+        return dtype == POLSAR_F32
+                   ? launch_window_kl_mma<float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end, radius,
+                                                        looks, h, workspace, out, s)
+                   : launch_window_kl_mma<double, double>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                          radius, looks, h, workspace, out, s);
     switch (dtype) {
         case POLSAR_F32:
             if (window_variant() == 4)

@@ -80,36 +80,96 @@ __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
         : "d"(a), "d"(b));
 }
 
-// One halo record from the 9 planes: Z, the doubled adjugate (Eq. 3), 1, D
-// (Eq. 6, the same det_eq6 as k_window_prep, so g is bit-identical to it).
-template <typename S, typename WT>
-__device__ __forceinline__ void mma_fill(double* rec, WT* gs, const S* __restrict__ z, int64_t ld, int64_t p,
-                                         bool in) {
-    double v[9];
+// Pair policies: fill() writes one halo slot's 20-double record (from the 9
+// planes) and its validity/g value; weight() maps the pair's dot product c to
+// the weight.  Invalid pixels (not positive definite, or non-finite) get a NaN
+// g, which the kernel turns into NaN W on every pixel whose window holds them
+// (R-19); out-of-image slots get g = 0 and are always masked.
+
+// The log-det window: record [Z, adj2, 1, D] (adjugate of Eq. 3, off-diagonal
+// entries doubled; D by Eq. 6, the same det_eq6 as k_window_prep, so g =
+// 1/(8D) is bit-identical to it); c = det(Z_i + Z_j).
+template <typename S_, typename WT_, bool A2_>
+struct MmaLogDet {
+    using S = S_;
+    using WT = WT_;
+    WT alpha;  // L / (2h): w = ((c/8)^2 / (D_i D_j))^-alpha
+    __device__ __forceinline__ static void fill(double* rec, WT* gs, const S* __restrict__ z, int64_t ld,
+                                                int64_t p, bool in) {
+        double v[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) v[k] = in ? (double)z[k * ld + p] : 0.0;
-    const double a = v[0], br = v[1], bi = v[2], cr = v[3], ci = v[4], d = v[5], er = v[6], ei = v[7],
-                 f = v[8];
-    const double A00 = FMA(d, f, -FMA(er, er, MUL(ei, ei)));
-    const double A01r = FMA(cr, er, FMA(ci, ei, -MUL(br, f)));   // c conj(e) - b f
-    const double A01i = FMA(ci, er, -FMA(cr, ei, MUL(bi, f)));
-    const double A02r = FMA(br, er, -FMA(bi, ei, MUL(cr, d)));   // b e - c d
-    const double A02i = FMA(br, ei, FMA(bi, er, -MUL(ci, d)));
-    const double A11 = FMA(a, f, -FMA(cr, cr, MUL(ci, ci)));
-    const double A12r = FMA(br, cr, FMA(bi, ci, -MUL(a, er)));   // conj(b) c - a e
-    const double A12i = FMA(br, ci, -FMA(bi, cr, MUL(a, ei)));
-    const double A22 = FMA(a, d, -FMA(br, br, MUL(bi, bi)));
-    const double D = det_eq6<double>(a, br, bi, cr, ci, d, er, ei, f);
-    const double r[MMA_RS] = {a,    br,         bi,         cr,         ci,         d,   er,
-                              ei,   f,          A00,        2.0 * A01r, 2.0 * A01i, 2.0 * A02r, 2.0 * A02i,
-                              A11,  2.0 * A12r, 2.0 * A12i, A22,        1.0,        D};
-    double2* o = reinterpret_cast<double2*>(rec);
+        for (int k = 0; k < 9; ++k) v[k] = in ? (double)z[k * ld + p] : 0.0;
+        const double a = v[0], br = v[1], bi = v[2], cr = v[3], ci = v[4], d = v[5], er = v[6], ei = v[7],
+                     f = v[8];
+        const double A00 = FMA(d, f, -FMA(er, er, MUL(ei, ei)));
+        const double A01r = FMA(cr, er, FMA(ci, ei, -MUL(br, f)));  // c conj(e) - b f
+        const double A01i = FMA(ci, er, -FMA(cr, ei, MUL(bi, f)));
+        const double A02r = FMA(br, er, -FMA(bi, ei, MUL(cr, d)));  // b e - c d
+        const double A02i = FMA(br, ei, FMA(bi, er, -MUL(ci, d)));
+        const double A11 = FMA(a, f, -FMA(cr, cr, MUL(ci, ci)));
+        const double A12r = FMA(br, cr, FMA(bi, ci, -MUL(a, er)));  // conj(b) c - a e
+        const double A12i = FMA(br, ci, -FMA(bi, cr, MUL(a, ei)));
+        const double A22 = FMA(a, d, -FMA(br, br, MUL(bi, bi)));
+        const double D = det_eq6<double>(a, br, bi, cr, ci, d, er, ei, f);
+        const double r[MMA_RS] = {a,    br,         bi,         cr,         ci,         d,   er,
+                                  ei,   f,          A00,        2.0 * A01r, 2.0 * A01i, 2.0 * A02r, 2.0 * A02i,
+                                  A11,  2.0 * A12r, 2.0 * A12i, A22,        1.0,        D};
+        double2* o = reinterpret_cast<double2*>(rec);
 #pragma unroll
-    for (int k = 0; k < MMA_RS / 2; ++k) o[k] = make_double2(r[2 * k], r[2 * k + 1]);
-    // g = 1 / (8 D) as k_window_prep (NaN marks a pixel that is not positive
-    // definite; 0 an out-of-image slot, never a valid pair)
-    const WT gv = (WT)(1.0 / MUL(8.0, D));
-    *gs = in ? ((D > 0.0 && gv < WT(INFINITY)) ? gv : WT(NAN)) : WT(0);
+        for (int k = 0; k < MMA_RS / 2; ++k) o[k] = make_double2(r[2 * k], r[2 * k + 1]);
+        const WT gv = (WT)(1.0 / MUL(8.0, D));
+        *gs = in ? ((D > 0.0 && gv < WT(INFINITY)) ? gv : WT(NAN)) : WT(0);
+    }
+    __device__ __forceinline__ WT weight(double c, WT gj, WT gi) const {
+        const WT fds = (WT)c;
+        const WT rr = (fds * gj) * (fds * gi);
+        return pair_weight(rr, alpha, A2_);
+    }
+};
+
+// The symmetric Wishart KL window (K6): record [Z, X, 1, -3] with X = w Z^-1
+// (Alg. 2, the Hermitian trace weights w as k_window_prep_kl), so
+// c = tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i) - 6 and d = L c / 2 (the -6 rides in the
+// dot product: no FP64 instruction outside the DMMAs).
+template <typename S_, typename WT_>
+struct MmaKL {
+    using S = S_;
+    using WT = WT_;
+    WT lk;  // L / h
+    __device__ __forceinline__ static void fill(double* rec, WT* gs, const S* __restrict__ z, int64_t ld,
+                                                int64_t p, bool in) {
+        H9<double> m;
+        double v[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) v[k] = in ? (double)z[k * ld + p] : 0.0;
+        m.a = v[0]; m.br = v[1]; m.bi = v[2]; m.cr = v[3]; m.ci = v[4];
+        m.d = v[5]; m.er = v[6]; m.ei = v[7]; m.f = v[8];
+        double x[9], det, t;
+        alg2_plain<double>(m, x, det, t);
+        const bool ok = det > 0.0 && t < INFINITY;
+        const double wk[9] = {1, 2, 2, 2, 2, 1, 2, 2, 1};
+        double r[MMA_RS];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            r[k] = v[k];
+            r[9 + k] = in ? (ok ? wk[k] * x[k] : (double)NAN) : 0.0;
+        }
+        r[18] = 1.0;
+        r[19] = -3.0;
+        double2* o = reinterpret_cast<double2*>(rec);
+#pragma unroll
+        for (int k = 0; k < MMA_RS / 2; ++k) o[k] = make_double2(r[2 * k], r[2 * k + 1]);
+        *gs = in ? (ok ? WT(1) : WT(NAN)) : WT(0);
+    }
+    __device__ __forceinline__ WT weight(double c, WT, WT) const;
+};
+template <>
+__device__ __forceinline__ float MmaKL<float, float>::weight(double c, float, float) const {
+    return fast_exp2(-lk * 0.5f * 1.4426950408889634f * (float)c);
+}
+template <>
+__device__ __forceinline__ double MmaKL<double, double>::weight(double c, double, double) const {
+    return exp(-lk * 0.5 * c);
 }
 
 // the owned operand's k -> record slot: [adj2, Z, D, 1] against the window
@@ -133,11 +193,11 @@ struct MmaLane {
 // DMMA, the weights into rp (forward) and the row's fixed-point sums into
 // the backward counters.  FULL: dy = wy - r in [1, R] for every r (no
 // branches, so the scheduler interleaves the chains).
-template <typename WT, bool A2, int NT, bool FULL>
-__device__ __forceinline__ void mma_row(const double* rec, const WT* gs, unsigned* ah, int HPe, int jrow,
-                                        const double (&bo)[MMA_RB][5], const WT (&gi)[MMA_RB][2],
-                                        const bool (&own)[MMA_RB][2], int wy, int R, WT alpha,
-                                        const MmaLane<WT>& ln, WT (&rp)[MMA_RB][2]) {
+template <typename Pair, int NT, bool FULL, typename WT = typename Pair::WT>
+__device__ __forceinline__ void mma_row(const Pair& pr, const double* rec, const WT* gs, unsigned* ah, int HPe,
+                                        int jrow, const double (&bo)[MMA_RB][5], const WT (&gi)[MMA_RB][2],
+                                        const bool (&own)[MMA_RB][2], int wy, int R, const MmaLane<WT>& ln,
+                                        WT (&rp)[MMA_RB][2]) {
 #pragma unroll
     for (int r = 0; r < MMA_RB; ++r) rp[r][0] = rp[r][1] = WT(0);
     long long vs[NT];
@@ -161,9 +221,7 @@ __device__ __forceinline__ void mma_row(const double* rec, const WT* gs, unsigne
             WT wb = WT(0);
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const WT fds = (WT)c[e];
-                const WT rr = (fds * gj) * (fds * gi[r][e]);
-                WT w = pair_weight(rr, alpha, A2);
+                WT w = pr.weight(c[e], gj, gi[r][e]);
                 w = ((m >> (2 * t + e)) & 1u) ? w : WT(0);
                 rp[r][e] += w;
                 wb += own[r][e] ? w : WT(0);
@@ -186,10 +244,13 @@ __device__ __forceinline__ void mma_row(const double* rec, const WT* gs, unsigne
     }
 }
 
-template <typename S, typename WT, bool A2, int NT>
+template <typename Pair, int NT>
 __global__ void __launch_bounds__(MMA_THREADS, 1)
-k_window_fwd_mma(const S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows, int64_t row_begin,
-                 int64_t row_end, int R, WT alpha, double* __restrict__ fbuf, long long* __restrict__ part) {
+k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
+                 int64_t row_begin, int64_t row_end, int R, double* __restrict__ fbuf,
+                 long long* __restrict__ part) {
+    using S = typename Pair::S;
+    using WT = typename Pair::WT;
     constexpr int TY = MMA_TY, RB = MMA_RB;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int HWe = K3_TX - 8 + 8 * NT;
@@ -205,7 +266,7 @@ k_window_fwd_mma(const S* __restrict__ z, int64_t ld, int64_t width, int64_t sla
         const int hy = q / HWe, hx = q % HWe;
         const int64_t gy = y0 + hy, gx = x0 - R + hx;
         const bool in = gy < slab_rows && gx >= 0 && gx < width;
-        mma_fill<S, WT>(rec + (size_t)MMA_RS * q, gs + q, z, ld, in ? gy * width + gx : 0, in);
+        Pair::fill(rec + (size_t)MMA_RS * q, gs + q, z, ld, in ? gy * width + gx : 0, in);
         ah[q] = 0u;
         ah[HPe + q] = 0u;
     }
@@ -268,9 +329,9 @@ k_window_fwd_mma(const S* __restrict__ z, int64_t ld, int64_t width, int64_t sla
         WT rp[RB][2];
         const int jrow = hy * HWe + 8 * cg;
         if (wy >= RB && wy <= R)  // every owned row sees this row at dy in [1, R]: no branches
-            mma_row<WT, A2, NT, true>(rec, gs, ah, HPe, jrow, bo, gi, own, wy, R, alpha, ln, rp);
+            mma_row<Pair, NT, true>(pr, rec, gs, ah, HPe, jrow, bo, gi, own, wy, R, ln, rp);
         else
-            mma_row<WT, A2, NT, false>(rec, gs, ah, HPe, jrow, bo, gi, own, wy, R, alpha, ln, rp);
+            mma_row<Pair, NT, false>(pr, rec, gs, ah, HPe, jrow, bo, gi, own, wy, R, ln, rp);
 #pragma unroll
         for (int r = 0; r < RB; ++r)
 #pragma unroll
@@ -311,47 +372,61 @@ inline size_t mma_sym_bytes(int64_t slab_rows, int64_t width, int R) {
     return acc_sym_bytes(0, slab_rows, width, R, MMA_TY);
 }
 
-template <typename S, typename WT, bool A2, int NT>
-int launch_fwd_mma(const S* z, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re, int R,
-                   WT alpha, double* fbuf, long long* part, cudaStream_t s) {
+template <typename Pair, int NT>
+int launch_fwd_mma(const Pair& pr, const typename Pair::S* z, int64_t ld, int64_t width, int64_t slab_rows,
+                   int64_t rb, int64_t re, int R, double* fbuf, long long* part, cudaStream_t s, const char* who) {
     const FwdGrid fg = fwd_grid(width, rb, re, R, MMA_TY);
-    const size_t smem = mma_fwd_smem<WT>(R);
-    auto kern = k_window_fwd_mma<S, WT, A2, NT>;
+    const size_t smem = mma_fwd_smem<typename Pair::WT>(R);
+    auto kern = k_window_fwd_mma<Pair, NT>;
     if (smem > K3_SMEM_MAX ||
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
+        return fail(POLSAR_ENOTSUP, who);
     dim3 grid((unsigned)fg.nbx, (unsigned)fg.nby);
-    kern<<<grid, MMA_THREADS, smem, s>>>(z, ld, width, slab_rows, fg.p0, re, R, alpha, fbuf, part);
+    kern<<<grid, MMA_THREADS, smem, s>>>(pr, z, ld, width, slab_rows, fg.p0, re, R, fbuf, part);
     return POLSAR_OK;
 }
 
-template <typename S, typename WT, bool A2>
-int launch_fwd_mma_r(const S* z, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re, int R,
-                     WT alpha, double* fbuf, long long* part, cudaStream_t s) {
-    switch (mma_nt(R)) {
-        case 1: return launch_fwd_mma<S, WT, A2, 1>(z, ld, width, slab_rows, rb, re, R, alpha, fbuf, part, s);
-        case 2: return launch_fwd_mma<S, WT, A2, 2>(z, ld, width, slab_rows, rb, re, R, alpha, fbuf, part, s);
-        case 3: return launch_fwd_mma<S, WT, A2, 3>(z, ld, width, slab_rows, rb, re, R, alpha, fbuf, part, s);
-        default: return launch_fwd_mma<S, WT, A2, 4>(z, ld, width, slab_rows, rb, re, R, alpha, fbuf, part, s);
-    }
-}
-
-// The log-det window, tensor-core pass 1 + pass 2 (R <= V3_RMAX).
-template <typename S, typename WT>
-int launch_window_mma(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re,
-                      int R, double looks, double h, void* wsv, void* outv, cudaStream_t s) {
+// Pass 1 (NT from R) + pass 2: workspace F | the tiles' backward sums (mma_sym_bytes).
+template <typename Pair>
+int launch_window_mma_pair(const Pair& pr, const void* zv, int64_t ld, int64_t width, int64_t slab_rows,
+                           int64_t rb, int64_t re, int R, void* wsv, void* outv, cudaStream_t s, const char* who) {
+    using S = typename Pair::S;
     const S* z = (const S*)zv;
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
     unsigned char* ws = (unsigned char*)wsv;
     double* fbuf = (double*)ws;
     long long* part = (long long*)(ws + up((size_t)slab_rows * width * sizeof(double)));
-    const double alpha = looks / (2.0 * h);
-    const int rc = alpha == 2.0
-                       ? launch_fwd_mma_r<S, WT, true>(z, ld, width, slab_rows, rb, re, R, (WT)alpha, fbuf, part, s)
-                       : launch_fwd_mma_r<S, WT, false>(z, ld, width, slab_rows, rb, re, R, (WT)alpha, fbuf, part, s);
+    int rc;
+    switch (mma_nt(R)) {
+        case 1: rc = launch_fwd_mma<Pair, 1>(pr, z, ld, width, slab_rows, rb, re, R, fbuf, part, s, who); break;
+        case 2: rc = launch_fwd_mma<Pair, 2>(pr, z, ld, width, slab_rows, rb, re, R, fbuf, part, s, who); break;
+        case 3: rc = launch_fwd_mma<Pair, 3>(pr, z, ld, width, slab_rows, rb, re, R, fbuf, part, s, who); break;
+        default: rc = launch_fwd_mma<Pair, 4>(pr, z, ld, width, slab_rows, rb, re, R, fbuf, part, s, who);
+    }
     if (rc != POLSAR_OK) return rc;
     launch_bwd_acc<S>(part, fbuf, width, rb, re, R, MMA_TY, outv, s);
-    return launch_check("polsar_window_distance: launch failed");
+    return launch_check(who);
+}
+
+// The log-det window (K3) with the tensor-core pass 1 (R <= V3_RMAX).
+template <typename S, typename WT>
+int launch_window_mma(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re,
+                      int R, double looks, double h, void* wsv, void* outv, cudaStream_t s) {
+    const double alpha = looks / (2.0 * h);
+    const char* who = "polsar_window_distance: tensor-core pass 1 failed";
+    if (alpha == 2.0)
+        return launch_window_mma_pair(MmaLogDet<S, WT, true>{(WT)alpha}, zv, ld, width, slab_rows, rb, re, R, wsv,
+                                      outv, s, who);
+    return launch_window_mma_pair(MmaLogDet<S, WT, false>{(WT)alpha}, zv, ld, width, slab_rows, rb, re, R, wsv,
+                                  outv, s, who);
+}
+
+// The KL window (K6) with the tensor-core pass 1 (R <= V3_RMAX).
+template <typename S, typename WT>
+int launch_window_kl_mma(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb, int64_t re,
+                         int R, double looks, double h, void* wsv, void* outv, cudaStream_t s) {
+    return launch_window_mma_pair(MmaKL<S, WT>{(WT)(looks / h)}, zv, ld, width, slab_rows, rb, re, R, wsv, outv, s,
+                                  "polsar_window_kl: tensor-core pass 1 failed");
 }
 
 }  // namespace

@@ -102,8 +102,9 @@ def test_window_workspace_covers_every_form(rows, width, radius):
     """polsar_window_workspace_bytes_for(entry) >= the need of every form that
     entry point may run: the weight planes (pitch rounded to 16
     bytes) for the NLM, the tiles' backward sums of the shared-memory form
-    (32-column tiles of 32 rows, or 24 / 16 for KL, each (32 + 2R)(TY + R)
-    int64) and the KL prepass; polsar_window_workspace_bytes >= all of them."""
+    (32-column tiles of 32 rows, or 24 / 16 for KL, or 8 for the tensor-core
+    pass 1, each (32 + 2R)(TY + R) int64) and the KL prepass;
+    polsar_window_workspace_bytes >= all of them."""
     lib = _lib.lib()
     up = lambda b: (b + 255) // 256 * 256  # noqa: E731
     n = rows * width
@@ -119,6 +120,9 @@ def test_window_workspace_covers_every_form(rows, width, radius):
             need[2] = [up(n * 160), acc(n * 160, 24 if wt == 4 else 16)]
             if radius == 12:
                 need[2].append(planes - up(n * wt) + up(n * 160))  # KL's plane form at R = 12
+        if dtype == 0:  # fp32 storage: the tensor-core pass 1 (8-row tiles, no prepass)
+            need[0].append(acc(0, 8))
+            need[2] = [acc(0, 8)]
         for e in range(3):
             got = lib.polsar_window_workspace_bytes_for(e, rows, width, radius, dtype)
             assert got >= max(need[e], default=0), (e, dtype, got, need[e])
