@@ -35,6 +35,13 @@ namespace {
 #ifndef POLSAR_MMA_TY
 #define POLSAR_MMA_TY 8
 #endif
+#ifndef POLSAR_MMA_PROBE
+#define POLSAR_MMA_PROBE 0  // development probe: 1 = tile fill and writeout only
+#endif
+#ifndef POLSAR_MMA_CHUNK
+#define POLSAR_MMA_CHUNK 16
+#endif
+constexpr int MMA_CHUNK = POLSAR_MMA_CHUNK;  // tiles per CTA (a column of them)
 constexpr int MMA_TY = POLSAR_MMA_TY;  // tile rows (pass 2 takes the same TY)
 constexpr int MMA_RB = 2;              // owned rows per warp
 constexpr int MMA_THREADS = 32 * (K3_TX / 8) * (MMA_TY / MMA_RB);  // one warp per 8 x RB pixels
@@ -68,10 +75,11 @@ __host__ __device__ constexpr int mma_nt(int R) { return (2 * R + 15) / 8; }
 // reach 2 columns past the window; those pairs are masked)
 __host__ __device__ constexpr int mma_hwe(int R) { return K3_TX - 8 + 8 * mma_nt(R); }
 
-template <typename WT>
+template <typename S, typename WT>
 size_t mma_fwd_smem(int R) {
     const size_t slots = (size_t)mma_hwe(R) * (MMA_TY + R);
-    return slots * (MMA_RS * sizeof(double) + sizeof(WT) + 2 * sizeof(unsigned));
+    return slots * (MMA_RS * sizeof(double) + sizeof(WT) + 2 * sizeof(unsigned)) +
+           (size_t)MMA_TY * mma_hwe(R) * 9 * sizeof(S);  // + the staging buffer
 }
 
 __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
@@ -94,11 +102,7 @@ struct MmaLogDet {
     using S = S_;
     using WT = WT_;
     WT alpha;  // L / (2h): w = ((c/8)^2 / (D_i D_j))^-alpha
-    __device__ __forceinline__ static void fill(double* rec, WT* gs, const S* __restrict__ z, int64_t ld,
-                                                int64_t p, bool in) {
-        double v[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) v[k] = in ? (double)z[k * ld + p] : 0.0;
+    __device__ __forceinline__ static void fill(double* rec, WT* gs, const double (&v)[9], bool in) {
         const double a = v[0], br = v[1], bi = v[2], cr = v[3], ci = v[4], d = v[5], er = v[6], ei = v[7],
                      f = v[8];
         const double A00 = FMA(d, f, -FMA(er, er, MUL(ei, ei)));
@@ -136,12 +140,8 @@ struct MmaKL {
     using S = S_;
     using WT = WT_;
     WT lk;  // L / h
-    __device__ __forceinline__ static void fill(double* rec, WT* gs, const S* __restrict__ z, int64_t ld,
-                                                int64_t p, bool in) {
+    __device__ __forceinline__ static void fill(double* rec, WT* gs, const double (&v)[9], bool in) {
         H9<double> m;
-        double v[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) v[k] = in ? (double)z[k * ld + p] : 0.0;
         m.a = v[0]; m.br = v[1]; m.bi = v[2]; m.cr = v[3]; m.ci = v[4];
         m.d = v[5]; m.er = v[6]; m.ei = v[7]; m.f = v[8];
         double x[9], det, t;
@@ -195,7 +195,7 @@ struct MmaLane {
 // branches, so the scheduler interleaves the chains).
 template <typename Pair, int NT, bool FULL, typename WT = typename Pair::WT>
 __device__ __forceinline__ void mma_row(const Pair& pr, const double* rec, const WT* gs, unsigned* ah, int HPe,
-                                        int jrow, const double (&bo)[MMA_RB][5], const WT (&gi)[MMA_RB][2],
+                                        int jrow, int jcnt, const double (&bo)[MMA_RB][5], const WT (&gi)[MMA_RB][2],
                                         const bool (&own)[MMA_RB][2], int wy, int R, const MmaLane<WT>& ln,
                                         WT (&rp)[MMA_RB][2]) {
 #pragma unroll
@@ -240,14 +240,29 @@ __device__ __forceinline__ void mma_row(const Pair& pr, const double* rec, const
     // block would split the row into basic blocks the scheduler cannot overlap)
     if (ln.kq == 0) {
 #pragma unroll
-        for (int t = 0; t < NT; ++t) acc_add(ah, HPe, jrow + 8 * t + ln.am, vs[t]);
+        for (int t = 0; t < NT; ++t) acc_add(ah, HPe, jcnt + 8 * t + ln.am, vs[t]);
     }
 }
 
+// ring row of tile row + offset, both < HH (no division)
+__device__ __forceinline__ int mma_ring(int r, int HH) { return r >= HH ? r - HH : r; }
+
+// cp.async of one plane element (4 or 8 bytes) into the staging buffer
+template <typename S>
+__device__ __forceinline__ void mma_cp_async(S* smem, const S* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sa), "l"(gmem), "n"(sizeof(S)) : "memory");
+}
+
+// Pass 1, persistent over a column of MMA_CHUNK tiles: tile by's halo rows
+// overlap tile by + 1's in HH - TY = R rows, so the records live in a ring of
+// HH rows and each later tile computes only its TY new rows -- from planes
+// that cp.async staged during the previous tile's DMMA work.  The backward-sum
+// counters are tile-relative: written out (and cleared) after each tile.
 template <typename Pair, int NT>
 __global__ void __launch_bounds__(MMA_THREADS, 1)
 k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, int64_t width, int64_t slab_rows,
-                 int64_t row_begin, int64_t row_end, int R, double* __restrict__ fbuf,
+                 int64_t row_begin, int64_t row_end, int R, int nby, double* __restrict__ fbuf,
                  long long* __restrict__ part) {
     using S = typename Pair::S;
     using WT = typename Pair::WT;
@@ -256,51 +271,22 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
     const int HWe = K3_TX - 8 + 8 * NT;
     const int HH = TY + R;
     const int HPe = HWe * HH;
+    const int HW = K3_TX + 2 * R;  // pass 2's tile layout
+    const int HP = HW * HH;
     double* rec = reinterpret_cast<double*>(smem_raw);
     WT* gs = reinterpret_cast<WT*>(rec + (size_t)MMA_RS * HPe);
-    unsigned* ah = reinterpret_cast<unsigned*>(gs + HPe);  // high counters, then low
+    unsigned* ah = reinterpret_cast<unsigned*>(gs + HPe);  // high counters, then low (tile-relative)
+    S* stg = reinterpret_cast<S*>(ah + 2 * HPe);           // staged planes of the next tile's TY new rows
 
     const int64_t x0 = (int64_t)blockIdx.x * K3_TX;
-    const int64_t y0 = row_begin + (int64_t)blockIdx.y * TY;
-    for (int q = threadIdx.x; q < HPe; q += blockDim.x) {
-        const int hy = q / HWe, hx = q % HWe;
-        const int64_t gy = y0 + hy, gx = x0 - R + hx;
-        const bool in = gy < slab_rows && gx >= 0 && gx < width;
-        Pair::fill(rec + (size_t)MMA_RS * q, gs + q, z, ld, in ? gy * width + gx : 0, in);
-        ah[q] = 0u;
-        ah[HPe + q] = 0u;
-    }
-    __syncthreads();
+    const int by0 = blockIdx.y * MMA_CHUNK;
+    const int by1 = by0 + MMA_CHUNK < nby ? by0 + MMA_CHUNK : nby;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int cg = warp % (K3_TX / 8), rg = warp / (K3_TX / 8);
     const int am = lane >> 2;  // A row (window pixel of a block) / B column (owned pixel of the B fragment)
     const int kq = lane & 3;   // fragment k / C column pair
     const int b0 = 2 * kq;     // this lane's C columns: owned pixels b0, b0 + 1
-
-    double bo[RB][5];
-    WT gi[RB][2];
-    bool own[RB][2];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        const int hr = (rg * RB + r) * HWe + R + 8 * cg;  // slot of the group's first owned pixel
-        const int64_t gy = y0 + rg * RB + r;
-#pragma unroll
-        for (int s = 0; s < 5; ++s) bo[r][s] = rec[(size_t)MMA_RS * (hr + am) + mma_perm(4 * s + kq)];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            gi[r][e] = gs[hr + b0 + e];
-            own[r][e] = x0 + 8 * cg + b0 + e < width && gy < row_end;
-        }
-        // rare: flag an invalid owned pixel and its forward targets (R-19)
-        const bool bad = x0 + 8 * cg + am < width && gy < row_end && !(gs[hr + am] > WT(0));
-        if (bad && kq == 0) {
-            const int qa = hr + am;
-            atomicOr(ah + HPe + qa, kBadBit);
-            for (int dy = 0; dy <= R; ++dy)
-                for (int dx = (dy == 0 ? 1 : -R); dx <= R; ++dx) atomicOr(ah + HPe + qa + dy * HWe + dx, kBadBit);
-        }
-    }
     // per-lane masks over (t, e): the window column test for dy > 0 and dy == 0,
     // and the image column test of the window pixel
     unsigned mfull = 0u, mzero = 0u;
@@ -315,55 +301,145 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
             mzero |= (unsigned)(col && dx >= 1 && dx <= R) << (2 * t + e);
         }
     }
-
-    // forward sums as fixed-point integers too (each row's float sum rounded
-    // to 2^-44): integer adds keep them off the FP64 pipe the DMMAs use
-    long long acc[RB][2];
-    unsigned fnan = 0u;  // (r, e) bits: a NaN weight entered that forward sum (R-19)
-#pragma unroll
-    for (int r = 0; r < RB; ++r) acc[r][0] = acc[r][1] = 0ll;
     const MmaLane<WT> ln{am, kq, b0, mfull, mzero};
-    for (int wy = 0; wy <= R + RB - 1; ++wy) {
-        const int hy = rg * RB + wy;
-        if (y0 + hy >= slab_rows) break;  // warp-uniform
-        WT rp[RB][2];
-        const int jrow = hy * HWe + 8 * cg;
-        if (wy >= RB && wy <= R)  // every owned row sees this row at dy in [1, R]: no branches
-            mma_row<Pair, NT, true>(pr, rec, gs, ah, HPe, jrow, bo, gi, own, wy, R, ln, rp);
-        else
-            mma_row<Pair, NT, false>(pr, rec, gs, ah, HPe, jrow, bo, gi, own, wy, R, ln, rp);
+
+    // the first tile: every halo row from global memory (all loads issued first)
+    {
+        constexpr int MAXQ = (56 * (MMA_TY + V3_RMAX) + MMA_THREADS - 1) / MMA_THREADS;
+        const int64_t y0 = row_begin + (int64_t)by0 * TY;
+        double v[MAXQ][9];
+        bool in[MAXQ];
+#pragma unroll
+        for (int i = 0; i < MAXQ; ++i) {
+            const int q = threadIdx.x + i * MMA_THREADS;
+            const int hy = q / HWe, hx = q % HWe;
+            const int64_t gy = y0 + hy, gx = x0 - R + hx;
+            in[i] = q < HPe && gy < slab_rows && gx >= 0 && gx < width;
+            const int64_t p = in[i] ? gy * width + gx : 0;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) v[i][k] = in[i] ? (double)z[k * ld + p] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < MAXQ; ++i) {
+            const int q = threadIdx.x + i * MMA_THREADS;
+            if (q < HPe) {
+                Pair::fill(rec + (size_t)MMA_RS * q, gs + q, v[i], in[i]);
+                ah[q] = 0u;
+                ah[HPe + q] = 0u;
+            }
+        }
+    }
+
+    for (int by = by0; by < by1; ++by) {
+        const int64_t y0 = row_begin + (int64_t)by * TY;
+        const int roff = ((by - by0) * TY) % HH;  // ring row of tile row 0
+        if (by > by0) {
+            // the TY new rows (tile rows R .. HH-1) from the staged planes; each
+            // thread fills the slots whose planes it staged itself
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            for (int q = threadIdx.x; q < TY * HWe; q += MMA_THREADS) {
+                const int hy = R + q / HWe, hx = q % HWe;
+                const int64_t gy = y0 + hy, gx = x0 - R + hx;
+                const bool in = gy < slab_rows && gx >= 0 && gx < width;
+                double v[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) v[k] = in ? (double)stg[q * 9 + k] : 0.0;
+                const int slot = mma_ring(hy + roff, HH) * HWe + hx;
+                Pair::fill(rec + (size_t)MMA_RS * slot, gs + slot, v, in);
+            }
+        }
+        __syncthreads();
+        // stage the next tile's new rows while this tile computes
+        if (by + 1 < by1) {
+            const int64_t yn = y0 + TY;  // the next tile's y0
+            for (int q = threadIdx.x; q < TY * HWe; q += MMA_THREADS) {
+                const int hy = R + q / HWe, hx = q % HWe;
+                const int64_t gy = yn + hy, gx = x0 - R + hx;
+                if (gy < slab_rows && gx >= 0 && gx < width) {
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) mma_cp_async(stg + q * 9 + k, z + k * ld + gy * width + gx);
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+
+        double bo[RB][5];
+        WT gi[RB][2];
+        bool own[RB][2];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            const int ty = rg * RB + r;
+            const int hr = mma_ring(ty + roff, HH) * HWe + R + 8 * cg;  // record slot of the group's first owned pixel
+            const int64_t gy = y0 + ty;
+#pragma unroll
+            for (int s = 0; s < 5; ++s) bo[r][s] = rec[(size_t)MMA_RS * (hr + am) + mma_perm(4 * s + kq)];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                gi[r][e] = gs[hr + b0 + e];
+                own[r][e] = x0 + 8 * cg + b0 + e < width && gy < row_end;
+            }
+            // rare: flag an invalid owned pixel and its forward targets (R-19)
+            const bool bad = x0 + 8 * cg + am < width && gy < row_end && !(gs[hr + am] > WT(0));
+            if (bad && kq == 0) {
+                const int qa = ty * HWe + R + 8 * cg + am;  // counter slot (tile-relative)
+                atomicOr(ah + HPe + qa, kBadBit);
+                for (int dy = 0; dy <= R; ++dy)
+                    for (int dx = (dy == 0 ? 1 : -R); dx <= R; ++dx)
+                        atomicOr(ah + HPe + qa + dy * HWe + dx, kBadBit);
+            }
+        }
+
+        // forward sums as fixed-point integers too (each row's float sum rounded
+        // to 2^-44): integer adds keep them off the FP64 datapath the DMMAs use
+        long long acc[RB][2];
+        unsigned fnan = 0u;  // (r, e) bits: a NaN weight entered that forward sum (R-19)
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acc[r][0] = acc[r][1] = 0ll;
+        for (int wy = 0; wy <= (POLSAR_MMA_PROBE ? -1 : R + RB - 1); ++wy) {
+            const int hy = rg * RB + wy;
+            if (y0 + hy >= slab_rows) break;  // warp-uniform
+            WT rp[RB][2];
+            const int jrow = mma_ring(hy + roff, HH) * HWe + 8 * cg;  // record slots (ring)
+            const int jcnt = hy * HWe + 8 * cg;                  // counter slots (tile-relative)
+            if (wy >= RB && wy <= R)  // every owned row sees this row at dy in [1, R]: no branches
+                mma_row<Pair, NT, true>(pr, rec, gs, ah, HPe, jrow, jcnt, bo, gi, own, wy, R, ln, rp);
+            else
+                mma_row<Pair, NT, false>(pr, rec, gs, ah, HPe, jrow, jcnt, bo, gi, own, wy, R, ln, rp);
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    acc[r][e] += fixed_w(rp[r][e]);
+                    fnan |= (unsigned)(rp[r][e] != rp[r][e]) << (2 * r + e);
+                }
+        }
+        // forward sums: the 8 lanes of a C column hold disjoint window pixels
 #pragma unroll
         for (int r = 0; r < RB; ++r)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                acc[r][e] += fixed_w(rp[r][e]);
-                fnan |= (unsigned)(rp[r][e] != rp[r][e]) << (2 * r + e);
+                long long a = acc[r][e];
+                a += __shfl_xor_sync(0xffffffffu, a, 4);
+                a += __shfl_xor_sync(0xffffffffu, a, 8);
+                a += __shfl_xor_sync(0xffffffffu, a, 16);
+                const unsigned nanl = __ballot_sync(0xffffffffu, (fnan >> (2 * r + e)) & 1u);
+                const bool isnan_f = (nanl & (0x11111111u << kq)) != 0u;
+                if (am == 0 && own[r][e])
+                    fbuf[(y0 + rg * RB + r) * width + x0 + 8 * cg + b0 + e] =
+                        isnan_f ? __longlong_as_double(0x7ff8000000000000ll) : (double)a * (1.0 / (double)kFix);
             }
-    }
-    // forward sums: the 8 lanes of a C column hold disjoint window pixels
-#pragma unroll
-    for (int r = 0; r < RB; ++r)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            long long a = acc[r][e];
-            a += __shfl_xor_sync(0xffffffffu, a, 4);
-            a += __shfl_xor_sync(0xffffffffu, a, 8);
-            a += __shfl_xor_sync(0xffffffffu, a, 16);
-            const unsigned nanl = __ballot_sync(0xffffffffu, (fnan >> (2 * r + e)) & 1u);
-            const bool isnan_f = (nanl & (0x11111111u << kq)) != 0u;
-            if (am == 0 && own[r][e])
-                fbuf[(y0 + rg * RB + r) * width + x0 + 8 * cg + b0 + e] =
-                    isnan_f ? __longlong_as_double(0x7ff8000000000000ll) : (double)a * (1.0 / (double)kFix);
+        __syncthreads();
+        // the tile's halo-region sums in pass 2's layout; each slot is cleared
+        // by the thread that writes it out (the columns HW..HWe-1 only ever hold
+        // zeros: masked pairs add 0, and no flag reaches past dx = R)
+        long long* dst = part + ((int64_t)by * gridDim.x + blockIdx.x) * HP;
+        for (int q = threadIdx.x; q < HP; q += MMA_THREADS) {
+            const int sq = (q / HW) * HWe + q % HW;
+            const unsigned hi = ah[sq], lo = ah[HPe + sq];
+            dst[q] = (lo & kBadBit) ? kBadSum : (long long)(((unsigned long long)hi << 22) + lo);
+            ah[sq] = 0u;
+            ah[HPe + sq] = 0u;
         }
-    __syncthreads();
-    // the tile's halo-region sums in pass 2's layout (HW = K3_TX + 2R columns)
-    const int HW = K3_TX + 2 * R;
-    const int HP = HW * HH;
-    long long* dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * HP;
-    for (int q = threadIdx.x; q < HP; q += blockDim.x) {
-        const int sq = (q / HW) * HWe + q % HW;
-        const unsigned lo = ah[HPe + sq];
-        dst[q] = (lo & kBadBit) ? kBadSum : (long long)(((unsigned long long)ah[sq] << 22) + lo);
     }
 }
 
@@ -376,13 +452,13 @@ template <typename Pair, int NT>
 int launch_fwd_mma(const Pair& pr, const typename Pair::S* z, int64_t ld, int64_t width, int64_t slab_rows,
                    int64_t rb, int64_t re, int R, double* fbuf, long long* part, cudaStream_t s, const char* who) {
     const FwdGrid fg = fwd_grid(width, rb, re, R, MMA_TY);
-    const size_t smem = mma_fwd_smem<typename Pair::WT>(R);
+    const size_t smem = mma_fwd_smem<typename Pair::S, typename Pair::WT>(R);
     auto kern = k_window_fwd_mma<Pair, NT>;
     if (smem > K3_SMEM_MAX ||
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return fail(POLSAR_ENOTSUP, who);
-    dim3 grid((unsigned)fg.nbx, (unsigned)fg.nby);
-    kern<<<grid, MMA_THREADS, smem, s>>>(pr, z, ld, width, slab_rows, fg.p0, re, R, fbuf, part);
+    dim3 grid((unsigned)fg.nbx, (unsigned)((fg.nby + MMA_CHUNK - 1) / MMA_CHUNK));
+    kern<<<grid, MMA_THREADS, smem, s>>>(pr, z, ld, width, slab_rows, fg.p0, re, R, fg.nby, fbuf, part);
     return POLSAR_OK;
 }
 
