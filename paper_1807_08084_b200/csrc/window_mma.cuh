@@ -27,6 +27,8 @@
 // (62.6 of 64 FMA/clk/SM at 16 warps, profiles/r01_micro_dmma_rate.txt)
 // against the scalar pair loop's 57 %.
 #pragma once
+#include <type_traits>
+
 #include "window_core.cuh"
 
 namespace polsar_impl {
@@ -41,7 +43,12 @@ namespace {
 #ifndef POLSAR_MMA_CHUNK
 #define POLSAR_MMA_CHUNK 16
 #endif
-constexpr int MMA_CHUNK = POLSAR_MMA_CHUNK;  // tiles per CTA (a column of them)
+constexpr int MMA_CHUNK = POLSAR_MMA_CHUNK;
+  // tiles per CTA (a column of them)
+#ifndef POLSAR_MMA_UNROLL
+#define POLSAR_MMA_UNROLL 1
+#endif
+constexpr int kMmaUnroll = POLSAR_MMA_UNROLL;  // full window rows per loop iteration
 constexpr int MMA_TY = POLSAR_MMA_TY;  // tile rows (pass 2 takes the same TY)
 constexpr int MMA_RB = 2;              // owned rows per warp
 constexpr int MMA_THREADS = 32 * (K3_TX / 8) * (MMA_TY / MMA_RB);  // one warp per 8 x RB pixels
@@ -395,16 +402,14 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
         unsigned fnan = 0u;  // (r, e) bits: a NaN weight entered that forward sum (R-19)
 #pragma unroll
         for (int r = 0; r < RB; ++r) acc[r][0] = acc[r][1] = 0ll;
-        for (int wy = 0; wy <= (POLSAR_MMA_PROBE ? -1 : R + RB - 1); ++wy) {
+        // window rows wy = hy - (first owned row): the full rows RB..R (every owned
+        // row at dy in [1, R]) in a loop of their own, the edge rows around it
+        auto row = [&](int wy, auto full) {
             const int hy = rg * RB + wy;
-            if (y0 + hy >= slab_rows) break;  // warp-uniform
             WT rp[RB][2];
             const int jrow = mma_ring(hy + roff, HH) * HWe + 8 * cg;  // record slots (ring)
-            const int jcnt = hy * HWe + 8 * cg;                  // counter slots (tile-relative)
-            if (wy >= RB && wy <= R)  // every owned row sees this row at dy in [1, R]: no branches
-                mma_row<Pair, NT, true>(pr, rec, gs, ah, HPe, jrow, jcnt, bo, gi, own, wy, R, ln, rp);
-            else
-                mma_row<Pair, NT, false>(pr, rec, gs, ah, HPe, jrow, jcnt, bo, gi, own, wy, R, ln, rp);
+            const int jcnt = hy * HWe + 8 * cg;                      // counter slots (tile-relative)
+            mma_row<Pair, NT, decltype(full)::value>(pr, rec, gs, ah, HPe, jrow, jcnt, bo, gi, own, wy, R, ln, rp);
 #pragma unroll
             for (int r = 0; r < RB; ++r)
 #pragma unroll
@@ -412,6 +417,15 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
                     acc[r][e] += fixed_w(rp[r][e]);
                     fnan |= (unsigned)(rp[r][e] != rp[r][e]) << (2 * r + e);
                 }
+        };
+        // (rows past the slab end are skipped: warp-uniform)
+        const int wmax = (int)(slab_rows - y0 - rg * RB - 1 < R + RB - 1 ? slab_rows - y0 - rg * RB - 1 : R + RB - 1);
+        if (!POLSAR_MMA_PROBE) {
+            for (int wy = 0; wy < RB && wy <= wmax; ++wy) row(wy, std::false_type{});
+            const int wf = R < wmax ? R : wmax;
+#pragma unroll kMmaUnroll
+            for (int wy = RB; wy <= wf; ++wy) row(wy, std::true_type{});
+            for (int wy = R + 1 > RB ? R + 1 : RB; wy <= wmax; ++wy) row(wy, std::false_type{});
         }
         // forward sums: the 8 lanes of a C column hold disjoint window pixels
 #pragma unroll
