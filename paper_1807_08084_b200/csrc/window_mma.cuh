@@ -203,7 +203,7 @@ struct MmaLane {
 template <typename Pair, int NT, bool FULL, typename WT = typename Pair::WT>
 __device__ __forceinline__ void mma_row(const Pair& pr, const double* rec, const WT* gs, unsigned* ah, int HPe,
                                         int jrow, int jcnt, const double (&bo)[MMA_RB][5], const WT (&gi)[MMA_RB][2],
-                                        const bool (&own)[MMA_RB][2], int wy, int R, const MmaLane<WT>& ln,
+                                        const unsigned (&mask)[MMA_RB][2], int wy, int R, const MmaLane<WT>& ln,
                                         WT (&rp)[MMA_RB][2]) {
 #pragma unroll
     for (int r = 0; r < MMA_RB; ++r) rp[r][0] = rp[r][1] = WT(0);
@@ -224,14 +224,16 @@ __device__ __forceinline__ void mma_row(const Pair& pr, const double* rec, const
             double c[2] = {0.0, 0.0};
 #pragma unroll
             for (int s = 0; s < 5; ++s) dmma_884(c, aw[s], bo[r][s]);
-            const unsigned m = (FULL || dy > 0) ? ln.mfull : ln.mzero;
+            // the window/image masks with the owned-pixel test folded in (the
+            // forward sums of pixels that are not owned are never written)
+            const unsigned m = (FULL || dy > 0) ? mask[r][0] : mask[r][1];
             WT wb = WT(0);
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 WT w = pr.weight(c[e], gj, gi[r][e]);
                 w = ((m >> (2 * t + e)) & 1u) ? w : WT(0);
                 rp[r][e] += w;
-                wb += own[r][e] ? w : WT(0);
+                wb += w;
             }
             // the two owned columns 2q, 2q+1 are fixed by x mod 8, so this
             // float sum is the same under any row decomposition; the rest is
@@ -396,6 +398,17 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
             }
         }
 
+        unsigned mask[RB][2];  // per owned row: (dy > 0, dy == 0) masks over (t, e), owned pixels only
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            unsigned ob = 0u;
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) ob |= (unsigned)own[r][e] << (2 * t + e);
+            mask[r][0] = mfull & ob;
+            mask[r][1] = mzero & ob;
+        }
         // forward sums as fixed-point integers too (each row's float sum rounded
         // to 2^-44): integer adds keep them off the FP64 datapath the DMMAs use
         long long acc[RB][2];
@@ -409,7 +422,7 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
             WT rp[RB][2];
             const int jrow = mma_ring(hy + roff, HH) * HWe + 8 * cg;  // record slots (ring)
             const int jcnt = hy * HWe + 8 * cg;                      // counter slots (tile-relative)
-            mma_row<Pair, NT, decltype(full)::value>(pr, rec, gs, ah, HPe, jrow, jcnt, bo, gi, own, wy, R, ln, rp);
+            mma_row<Pair, NT, decltype(full)::value>(pr, rec, gs, ah, HPe, jrow, jcnt, bo, gi, mask, wy, R, ln, rp);
 #pragma unroll
             for (int r = 0; r < RB; ++r)
 #pragma unroll
