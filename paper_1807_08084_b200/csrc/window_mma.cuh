@@ -66,16 +66,6 @@ int window_mma_mode() {
     return v;
 }
 
-// Does polsar_window_distance run the tensor-core form for this call?  (The
-// workspace query asks the same question.)  The other A/B forms
-// (POLSAR_WINDOW_VARIANT=2/3, POLSAR_WINDOW_PLANES=1) take precedence.
-bool use_window_mma(int dtype, int radius) {
-    if (radius > V3_RMAX || window_variant() != 4 || window_planes()) return false;
-    const int m = window_mma_mode();
-    if (m == 0) return false;
-    if (dtype == POLSAR_F32) return true;
-    return m == 1 && (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN);
-}
 
 __host__ __device__ constexpr int mma_nt(int R) { return (2 * R + 15) / 8; }
 // halo columns: x0 - R .. x0 - R + HWe - 1 (the last group's NT blocks may
@@ -87,6 +77,18 @@ size_t mma_fwd_smem(int R) {
     const size_t slots = (size_t)mma_hwe(R) * (MMA_TY + R);
     return slots * (MMA_RS * sizeof(double) + sizeof(WT) + 2 * sizeof(unsigned)) +
            (size_t)MMA_TY * mma_hwe(R) * 9 * sizeof(S);  // + the staging buffer
+}
+
+// Does polsar_window_distance run the tensor-core form for this call?  (The
+// workspace query asks the same question.)  The other A/B forms
+// (POLSAR_WINDOW_VARIANT=2/3, POLSAR_WINDOW_PLANES=1) take precedence.
+bool use_window_mma(int dtype, int radius) {
+    if (radius > V3_RMAX || window_variant() != 4 || window_planes()) return false;
+    const int m = window_mma_mode();
+    if (m == 0) return false;
+    if (dtype == POLSAR_F32) return mma_fwd_smem<float, float>(radius) <= K3_SMEM_MAX;
+    return m == 1 && (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) &&
+           mma_fwd_smem<double, double>(radius) <= K3_SMEM_MAX;  // (fp64 at R = 12 does not fit)
 }
 
 __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {

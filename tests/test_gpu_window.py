@@ -128,6 +128,13 @@ for dt, tol, tol_kl in ((torch.float32, 2e-5, 2e-5), (torch.float64, 4e-10, 2e-9
     ref = oracle.window_kl(z.cpu().numpy(), h, w, r, 4.0, 1.0)
     e = float((np.abs(got - ref) / ref).max())
     assert e <= tol_kl, ("kl", dt, e)
+    # R = 12 (the tensor-core form's largest tile; fp64 falls back to the scalar form)
+    h, w = 40, 45
+    z = wishart.generate(configs.get("c5").scaled(h, w), device="cuda").to(dt)
+    got = P.window_distance(z, h, w, radius=12).cpu().numpy()
+    ref = oracle.window(z.cpu().numpy(), h, w, 12, 4.0, 1.0)
+    e = float((np.abs(got - ref) / ref).max())
+    assert e <= tol, ("window R=12", dt, e)
 print("ok")
 '''
     env = dict(os.environ, **VARIANT_ENV[variant])
