@@ -213,6 +213,7 @@ __device__ __forceinline__ void mma_row(const Pair& pr, const double* rec, const
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
         const int jb = jrow + 8 * t;  // slot of the block's first window pixel
+        POLSAR_CHECK(jb + ln.am >= 0 && jb + ln.am < HPe && jcnt + 8 * t + ln.am < HPe);
         const double* ra = rec + (size_t)MMA_RS * (jb + ln.am) + ln.kq;
         double aw[5];
 #pragma unroll
@@ -356,6 +357,7 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
 #pragma unroll
                 for (int k = 0; k < 9; ++k) v[k] = in ? (double)stg[q * 9 + k] : 0.0;
                 const int slot = mma_ring(hy + roff, HH) * HWe + hx;
+                POLSAR_CHECK(slot >= 0 && slot < HPe && q * 9 + 8 < MMA_TY * HWe * 9);
                 Pair::fill(rec + (size_t)MMA_RS * slot, gs + slot, v, in);
             }
         }
@@ -381,6 +383,7 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
         for (int r = 0; r < RB; ++r) {
             const int ty = rg * RB + r;
             const int hr = mma_ring(ty + roff, HH) * HWe + R + 8 * cg;  // record slot of the group's first owned pixel
+            POLSAR_CHECK(hr + 7 < HPe && roff >= 0 && roff < HH);
             const int64_t gy = y0 + ty;
 #pragma unroll
             for (int s = 0; s < 5; ++s) bo[r][s] = rec[(size_t)MMA_RS * (hr + am) + mma_perm(4 * s + kq)];
@@ -393,6 +396,7 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
             const bool bad = x0 + 8 * cg + am < width && gy < row_end && !(gs[hr + am] > WT(0));
             if (bad && kq == 0) {
                 const int qa = ty * HWe + R + 8 * cg + am;  // counter slot (tile-relative)
+                POLSAR_CHECK(qa - R >= 0 && qa + R * HWe + R < HPe);
                 atomicOr(ah + HPe + qa, kBadBit);
                 for (int dy = 0; dy <= R; ++dy)
                     for (int dx = (dy == 0 ? 1 : -R); dx <= R; ++dx)
@@ -464,6 +468,7 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
         long long* dst = part + ((int64_t)by * gridDim.x + blockIdx.x) * HP;
         for (int q = threadIdx.x; q < HP; q += MMA_THREADS) {
             const int sq = (q / HW) * HWe + q % HW;
+            POLSAR_CHECK(sq < HPe);
             const unsigned hi = ah[sq], lo = ah[HPe + sq];
             dst[q] = (lo & kBadBit) ? kBadSum : (long long)(((unsigned long long)hi << 22) + lo);
             ah[sq] = 0u;
