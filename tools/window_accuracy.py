@@ -40,17 +40,19 @@ def main():
 
     ref = oracle.window_threaded(zh, h, w, R, cfg.looks, cfg.h, idx, threads)
     ii = torch.as_tensor(idx, device=dev)
+    mma = os.environ.get("POLSAR_WINDOW_MMA", "") != "0"  # (read once per process by the library too)
+    form = "tensor-core pass 1" if mma else "scalar pass 1"
     for plain in (False, True):
         got = P.window_distance(z, h, w, radius=R, looks=cfg.looks, h=cfg.h, plain=plain)[ii].cpu().numpy()
         row("window W", "fp32 storage, fp32 pair det (plain; reported)" if plain else
-            "fp32 storage, fp64 pair det (default)", "none" if plain else "2e-5", np.abs(got - ref) / ref)
+            f"fp32 storage, fp64 pair det ({form})", "none" if plain else "2e-5", np.abs(got - ref) / ref)
     z64 = z.double()
     got = P.window_distance(z64, h, w, radius=R, looks=cfg.looks, h=cfg.h)[ii].cpu().numpy()
     ref64 = oracle.window_threaded(z64.cpu().numpy(), h, w, R, cfg.looks, cfg.h, idx, threads)
     row("window W", "fp64 storage", "4e-10", np.abs(got - ref64) / ref64)
     refk = oracle.window_kl_threaded(zh, h, w, R, cfg.looks, cfg.h, idx, threads)
     got = P.window_kl(z, h, w, radius=R, looks=cfg.looks, h=cfg.h)[ii].cpu().numpy()
-    row("KL window W", "fp32 storage, fp64 trace products", "2e-5", np.abs(got - refk) / refk)
+    row("KL window W", f"fp32 storage, fp64 trace products ({form})", "2e-5", np.abs(got - refk) / refk)
     zhat, W = P.nlm_filter(z, h, w, radius=R, looks=cfg.looks, h=cfg.h)
     rz, rw = oracle.nlm_threaded(zh, h, w, R, cfg.looks, cfg.h, idx, threads)
     gz = zhat[:, ii].cpu().numpy().astype(np.float64)
