@@ -1,5 +1,6 @@
 // window_mma.cuh -- part of libpolsar.so (B200, sm_100a); arXiv 1807.08084.
-// K3b pass 1 on the FP64 tensor cores (default for fp32 storage; POLSAR_WINDOW_MMA).
+// Pass 1 of the window sums on the FP64 tensor cores: K3b (log-det distance)
+// and K6 (symmetric Wishart KL), the default for fp32 storage (POLSAR_WINDOW_MMA).
 //
 // The pair determinant of the log-det window (BASELINE
 // configs[4]) through the 3x3 identity
@@ -9,23 +10,26 @@
 //   a_i = [adj2(Z_i), Z_i, D_i, 1],   b_j = [Z_j, adj2(Z_j), 1, D_j],
 // adj2 = the adjugate of Eq. 3 with its off-diagonal entries doubled (the
 // Hermitian inner product counts each off-diagonal pair twice), D = det by
-// Eq. 6.  So an 8 x 8 block of pair determinants (8 owned pixels of a row x 8
-// window pixels of a row) is one 8 x 8 x 20 fp64 matrix product: five
-// mma.sync.m8n8k4.f64 (DMMA).  Each warp keeps the a-fragments of its
-// 2 rows x 8 pixels in registers (5 doubles per row per lane) and streams the
-// b-fragments of the window rows from shared memory.  The symmetric two-pass
-// structure of the ACC form (window_core.cuh) is kept: pass 1 covers the
-// forward half-window (dy = 1..R, and dy = 0 with dx = 1..R) and adds every
-// weight to the neighbour's fixed-point backward sum in shared memory; pass 2
-// is k_window_bwd_acc unchanged (tile height 8).
+// Eq. 6.  So an 8 x 8 block of pair determinants (8 window pixels of a row x
+// 8 owned pixels of a row) is one 8 x 8 x 20 fp64 matrix product: five
+// mma.sync.m8n8k4.f64 (DMMA).  The KL distance's T - 6 = <X_i, Z_j> +
+// <Z_i, X_j> - 6 (X = w Z^-1, Alg. 2) has the same shape (MmaKL).  Each warp
+// keeps the fragments of its 2 rows x 8 owned pixels in registers (the B
+// operand: 5 doubles per row per lane) and streams the window pixels' records
+// from shared memory (the A operand).  The symmetric two-pass structure of
+// the ACC form (window_core.cuh) is kept: pass 1 covers the forward
+// half-window (dy = 1..R, and dy = 0 with dx = 1..R) and adds every weight to
+// the neighbour's fixed-point backward sum in shared memory; pass 2 is
+// k_window_bwd_acc unchanged (tile height 8).  A CTA walks a column of
+// MMA_CHUNK tiles with the halo records in a ring (k_window_fwd_mma).
 //
 // Per 8-pixel group and window row the 8 + 2R window columns are covered by
 // NT = ceil((8 + 2R) / 8) column blocks of 8 (72 % of the computed pairs are
 // inside the window at R = 11): 47 blocks x 5 DMMA x 256 FMA per 8 pixels, an
 // FP64 floor of 1.69 ms at c5, the same as the scalar form's 29 operations per
-// pair (1.72 ms) -- the gain sought is the tensor pipe's issue efficiency
-// (62.6 of 64 FMA/clk/SM at 16 warps, profiles/r01_micro_dmma_rate.txt)
-// against the scalar pair loop's 57 %.
+// pair (1.72 ms) -- the gain is the tensor pipe's issue efficiency (62.6 of
+// 64 FMA/clk/SM at 16 warps, profiles/r01_micro_dmma_rate.txt; 67 % busy in
+// this kernel) against the scalar pair loop's 57 % of the FP64 pipe.
 #pragma once
 #include <type_traits>
 
@@ -43,8 +47,7 @@ namespace {
 #ifndef POLSAR_MMA_CHUNK
 #define POLSAR_MMA_CHUNK 16
 #endif
-constexpr int MMA_CHUNK = POLSAR_MMA_CHUNK;
-  // tiles per CTA (a column of them)
+constexpr int MMA_CHUNK = POLSAR_MMA_CHUNK;  // tiles per CTA (a column of them)
 #ifndef POLSAR_MMA_UNROLL
 #define POLSAR_MMA_UNROLL 1
 #endif
