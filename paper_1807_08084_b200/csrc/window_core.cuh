@@ -1205,22 +1205,23 @@ __global__ void __launch_bounds__(256)
 k_window_bwd_acc(const long long* __restrict__ part, const double* __restrict__ fbuf, int64_t width,
                  int64_t row_begin, int64_t row_end, int64_t p0, int R, int TY, int nbx, int nby,
                  S* __restrict__ out) {
+    // a 2D grid (columns x rows, rows grid-strided): no 64-bit division per pixel
     const int HW = K3_TX + 2 * R;
     const int HP = HW * (TY + R);
-    const int64_t m = (row_end - row_begin) * width;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t y = row_begin + q / width, x = q % width;
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= width) return;
+    // bx: 32 bx - R <= x < 32 bx + 32 + R
+    const int bx_hi = (int)((x + R) / K3_TX < nbx - 1 ? (x + R) / K3_TX : nbx - 1);
+    const int bx_lo = (int)(x - K3_TX - R + 1 > 0 ? (x - K3_TX - R + 1 + K3_TX - 1) / K3_TX : 0);
+    for (int64_t y = row_begin + blockIdx.y; y < row_end; y += gridDim.y) {
         const int64_t yr = y - p0;  // >= 0
-        // by: p0 + by TY <= y < p0 + by TY + TY + R ; bx: 32 bx - R <= x < 32 bx + 32 + R
+        // by: p0 + by TY <= y < p0 + by TY + TY + R
         const int64_t by_hi = yr / TY;
         const int64_t by_lo = yr - TY - R + 1 > 0 ? (yr - TY - R + 1 + TY - 1) / TY : 0;
-        const int64_t bx_hi = (x + R) / K3_TX < nbx - 1 ? (x + R) / K3_TX : nbx - 1;
-        const int64_t bx_lo = x - K3_TX - R + 1 > 0 ? (x - K3_TX - R + 1 + K3_TX - 1) / K3_TX : 0;
         long long sum = 0;
         bool bad = false;
         for (int64_t by = by_lo; by <= by_hi && by < nby; ++by)
-            for (int64_t bx = bx_lo; bx <= bx_hi; ++bx) {
+            for (int bx = bx_lo; bx <= bx_hi; ++bx) {
                 const int64_t hy = yr - by * TY, hx = x - K3_TX * bx + R;
                 POLSAR_CHECK(hy >= 0 && hy < TY + R && hx >= 0 && hx < HW);
                 const long long t = part[(by * nbx + bx) * HP + hy * HW + hx];
@@ -1228,7 +1229,7 @@ k_window_bwd_acc(const long long* __restrict__ part, const double* __restrict__ 
                 sum += t;
             }
         const double wb = bad ? __longlong_as_double(0x7ff8000000000000ll) : (double)sum * (1.0 / (double)kFix);
-        out[q] = (S)__dadd_rn(__dadd_rn(1.0, fbuf[y * width + x]), wb);
+        out[(y - row_begin) * width + x] = (S)__dadd_rn(__dadd_rn(1.0, fbuf[y * width + x]), wb);
     }
 }
 
@@ -1320,8 +1321,10 @@ template <typename S>
 void launch_bwd_acc(const long long* part, const double* fbuf, int64_t width, int64_t rb, int64_t re,
                     int R, int TY, void* outv, cudaStream_t s) {
     const FwdGrid fg = fwd_grid(width, rb, re, R, TY);
-    k_window_bwd_acc<S><<<grid_for((re - rb) * width, 256), 256, 0, s>>>(part, fbuf, width, rb, re, fg.p0, R,
-                                                                        TY, fg.nbx, fg.nby, (S*)outv);
+    const int64_t rows = re - rb;
+    if (rows <= 0 || width <= 0) return;
+    dim3 grid((unsigned)((width + 255) / 256), (unsigned)(rows < 65535 ? rows : 65535));
+    k_window_bwd_acc<S><<<grid, 256, 0, s>>>(part, fbuf, width, rb, re, fg.p0, R, TY, fg.nbx, fg.nby, (S*)outv);
 }
 
 // workspace of the ACC forms: the prepass planes (pre_bytes) | F | the tiles'
