@@ -14,6 +14,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "alg.cuh"
 
@@ -1131,58 +1132,71 @@ k_window_fwd(Pair pr, int64_t width, int64_t slab_rows, int64_t row_begin, int64
         }
     }
 
-    for (int wy = 0; wy <= R + RB - 1; ++wy) {
-        const int64_t gyj = y0 + ty0 + wy;
-        if (gyj >= slab_rows) break;  // warp-uniform
+    // window rows wy: the full rows RB..R (every owned pixel at dy = wy - r in
+    // [1, R]) in loops of their own (no per-row branch between the full and the
+    // edge forms; measured on the tensor-core pass 1), the edge rows around them
+    auto full_row = [&](int wy, auto fullc) {
         const int hy = ty0 + wy;
         const T* rec = sz + RS * (hy * HW + tx);  // neighbour wx = -R
         WT row[RB];
 #pragma unroll
         for (int r = 0; r < RB; ++r) row[r] = WT(0);
-        if (wy >= RB && wy <= R) {
-            // every owned pixel sees this row at dy = wy - r in [1, R]: full rows.
-            // wp[r] walks the weight planes delta = (wy - r, wx), consecutive in wx.
-            WT* wp[RB];
+        // wp[r] walks the weight planes delta = (wy - r, wx), consecutive in wx.
+        WT* wp[RB];
 #pragma unroll
-            for (int r = 0; r < RB; ++r) wp[r] = wbuf + (int64_t)fwd_index(wy - r, -R, R) * N + pi[r];
-            POLSAR_CHECK(hy >= 0 && hy < HH && tx + 2 * R < HW);  // records wx = -R..R
-            const int qj = hy * HW + tx;  // backward-sum slot of neighbour wx = -R
-            if constexpr (Pair::kPipeline)
-                fwd_full_row_pipelined<Pair, RB, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row,
-                                                      ah, HP, qj);
-            else if (full)
-                fwd_full_row<Pair, RB, true, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row,
-                                                  ah, HP, qj);
-            else
-                fwd_full_row<Pair, RB, false, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row,
-                                                   ah, HP, qj);
-        } else {
-            for (int wx = -R; wx <= R; ++wx, rec += RS) {
-                POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
-                Rec rj;
-                Pair::load(rec, rj);
-                const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-                long long v = 0;
+        for (int r = 0; r < RB; ++r) wp[r] = wbuf + (int64_t)fwd_index(wy - r, -R, R) * N + pi[r];
+        POLSAR_CHECK(hy >= 0 && hy < HH && tx + 2 * R < HW);  // records wx = -R..R
+        const int qj = hy * HW + tx;  // backward-sum slot of neighbour wx = -R
+        if constexpr (Pair::kPipeline)
+            fwd_full_row_pipelined<Pair, RB, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N, row, ah, HP,
+                                                  qj);
+        else
+            fwd_full_row<Pair, RB, decltype(fullc)::value, ACC>(pr, ri, rec, R, gx, width, interior_x, own, wp, N,
+                                                                 row, ah, HP, qj);
 #pragma unroll
-                for (int r = 0; r < RB; ++r) {
-                    const int dy = wy - r;
-                    if (dy >= 0 && dy <= R && (dy > 0 || wx > 0)) {  // warp-uniform
-                        WT w = pr.weight(ri[r], rj);
-                        w = colok ? w : WT(0);
-                        row[r] += w;
-                        if constexpr (ACC) {
-                            if (own[r]) v += fixed_w(w);
-                        } else {
-                            if (colok && own[r]) wbuf[(int64_t)fwd_index(dy, wx, R) * N + pi[r]] = w;
-                        }
+        for (int r = 0; r < RB; ++r) acc[r] += (double)row[r];
+    };
+    auto edge_row = [&](int wy) {
+        const int hy = ty0 + wy;
+        const T* rec = sz + RS * (hy * HW + tx);  // neighbour wx = -R
+        WT row[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) row[r] = WT(0);
+        for (int wx = -R; wx <= R; ++wx, rec += RS) {
+            POLSAR_CHECK(hy >= 0 && hy < HH && tx + wx + R >= 0 && tx + wx + R < HW);
+            Rec rj;
+            Pair::load(rec, rj);
+            const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
+            long long v = 0;
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                const int dy = wy - r;
+                if (dy >= 0 && dy <= R && (dy > 0 || wx > 0)) {  // warp-uniform
+                    WT w = pr.weight(ri[r], rj);
+                    w = colok ? w : WT(0);
+                    row[r] += w;
+                    if constexpr (ACC) {
+                        if (own[r]) v += fixed_w(w);
+                    } else {
+                        if (colok && own[r]) wbuf[(int64_t)fwd_index(dy, wx, R) * N + pi[r]] = w;
                     }
                 }
-                if constexpr (ACC) acc_add(ah, HP, hy * HW + tx + wx + R, v);
             }
+            if constexpr (ACC) acc_add(ah, HP, hy * HW + tx + wx + R, v);
         }
 #pragma unroll
         for (int r = 0; r < RB; ++r) acc[r] += (double)row[r];
+    };
+    // (rows past the slab end are skipped: warp-uniform)
+    const int wmax = (int)(slab_rows - y0 - ty0 - 1 < R + RB - 1 ? slab_rows - y0 - ty0 - 1 : R + RB - 1);
+    for (int wy = 0; wy < RB && wy <= wmax; ++wy) edge_row(wy);
+    const int wf = R < wmax ? R : wmax;
+    if (full) {
+        for (int wy = RB; wy <= wf; ++wy) full_row(wy, std::true_type{});
+    } else {
+        for (int wy = RB; wy <= wf; ++wy) full_row(wy, std::false_type{});
     }
+    for (int wy = R + 1 > RB ? R + 1 : RB; wy <= wmax; ++wy) edge_row(wy);
 #pragma unroll
     for (int r = 0; r < RB; ++r)
         if (gx < width && y0 + ty0 + r < row_end) fbuf[(y0 + ty0 + r) * width + gx] = acc[r];
