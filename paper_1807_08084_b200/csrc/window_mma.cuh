@@ -42,7 +42,7 @@ namespace {
 #define POLSAR_MMA_TY 8
 #endif
 #ifndef POLSAR_MMA_PROBE
-#define POLSAR_MMA_PROBE 0  // development probe: 1 = tile fill and writeout only
+#define POLSAR_MMA_PROBE 0  // development probe: 1 = tile fill and writeout only; 2 = no weight arithmetic
 #endif
 #ifndef POLSAR_MMA_CHUNK
 #define POLSAR_MMA_CHUNK 16
@@ -137,6 +137,9 @@ struct MmaLogDet {
         *gs = in ? ((D > 0.0 && gv < WT(INFINITY)) ? gv : WT(NAN)) : WT(0);
     }
     __device__ __forceinline__ WT weight(double c, WT gj, WT gi) const {
+#if POLSAR_MMA_PROBE == 2
+        return (WT)c * gi;  // development probe: the epilogue without the weight arithmetic
+#endif
         const WT fds = (WT)c;
         const WT rr = (fds * gj) * (fds * gi);
         return pair_weight(rr, alpha, A2_);
@@ -442,7 +445,7 @@ k_window_fwd_mma(Pair pr, const typename Pair::S* __restrict__ z, int64_t ld, in
         };
         // (rows past the slab end are skipped: warp-uniform)
         const int wmax = (int)(slab_rows - y0 - rg * RB - 1 < R + RB - 1 ? slab_rows - y0 - rg * RB - 1 : R + RB - 1);
-        if (!POLSAR_MMA_PROBE) {
+        if (POLSAR_MMA_PROBE != 1) {
             for (int wy = 0; wy < RB && wy <= wmax; ++wy) row(wy, std::false_type{});
             const int wf = R < wmax ? R : wmax;
 #pragma unroll kMmaUnroll
