@@ -53,7 +53,10 @@ constexpr int MMA_CHUNK = POLSAR_MMA_CHUNK;  // tiles per CTA (a column of them)
 #endif
 constexpr int kMmaUnroll = POLSAR_MMA_UNROLL;  // full window rows per loop iteration
 constexpr int MMA_TY = POLSAR_MMA_TY;  // tile rows (pass 2 takes the same TY)
-constexpr int MMA_RB = 2;              // owned rows per warp
+#ifndef POLSAR_MMA_RB
+#define POLSAR_MMA_RB 2
+#endif
+constexpr int MMA_RB = POLSAR_MMA_RB;  // owned rows per warp
 constexpr int MMA_THREADS = 32 * (K3_TX / 8) * (MMA_TY / MMA_RB);  // one warp per 8 x RB pixels
 constexpr int MMA_RS = 20;             // record doubles: Z (9) | adj2 (9) | 1 | D  (160 B:
                                        // a warp's b-fragment loads hit 32 distinct banks per half)
