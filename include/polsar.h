@@ -200,8 +200,13 @@ int polsar_checksum(const void* planes, int64_t n, int64_t ld, int nplanes, int 
  *   dev_ws   : device workspace of ws_bytes; the chunk size is derived from it
  *              (polsar_host_chunk_pixels; 256-byte aligned pointer required).
  *   stream_h2d, stream_compute, stream_d2h : three distinct CUDA streams.
- * Synchronous: returns after the last D2H copy has completed (the only
- * entry point that synchronises, on stream_d2h). */
+ * Host planes whose stride ld_host * element size exceeds the device's
+ * cudaDevAttrMaxPitch (2^31 - 1 B) are copied plane by plane instead of by
+ * one 2D copy per chunk.  Pageable host memory works, at pageable speed.
+ * Synchronous: returns after the last D2H copy has completed; on every path,
+ * error paths included, it first synchronises all three streams, so nothing
+ * it enqueued still touches the host buffers or dev_ws (the only entry point
+ * that synchronises). */
 int polsar_inv_det_host(const void* z_host, void* out_host, uint8_t* status_host, int64_t n,
                         int64_t ld_host, int dtype, int algo, void* dev_ws, size_t ws_bytes,
                         void* stream_h2d, void* stream_compute, void* stream_d2h);

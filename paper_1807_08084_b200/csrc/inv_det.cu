@@ -472,15 +472,31 @@ int polsar_inv_det_host(const void* z_host, void* out_host, uint8_t* status_host
     if (chunk <= 0) return fail(POLSAR_EINVAL, "workspace too small");
     cudaStream_t sh = (cudaStream_t)stream_h2d, sc = (cudaStream_t)stream_compute,
                  sd = (cudaStream_t)stream_d2h;
+    // 2D copies take the host plane stride as their pitch, which CUDA caps at
+    // cudaDevAttrMaxPitch (2^31 - 1 B): a plane stride beyond it (fp64 with
+    // ld_host >= 2^28, e.g. a UAVSAR-scale c4 image) is copied plane by plane.
+    int dev = 0, max_pitch = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_pitch, cudaDevAttrMaxPitch, dev) != cudaSuccess)
+        return fail(POLSAR_ECUDA, "polsar_inv_det_host: device query failed");
+    const bool use_2d = (uint64_t)ld_host * es <= (uint64_t)max_pitch;
+    auto copy_planes = [&](void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                           int planes, cudaMemcpyKind kind, cudaStream_t st) -> bool {
+        if (use_2d) return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, planes, kind, st) == cudaSuccess;
+        for (int k = 0; k < planes; ++k)
+            if (cudaMemcpyAsync((unsigned char*)dst + k * dpitch, (const unsigned char*)src + k * spitch,
+                                width, kind, st) != cudaSuccess)
+                return false;
+        return true;
+    };
     // slot layout: [9 in planes][11 out planes][status], each plane `chunk` elements
     const size_t slot_bytes = (size_t)chunk * (20 * es + 1);
-    cudaEvent_t ev_in[3], ev_k[3], ev_out[3];
-    for (int i = 0; i < 3; ++i) {
-        cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_k[i], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming);
-    }
-    int rc = POLSAR_OK;
+    cudaEvent_t ev[9];
+    int n_ev = 0;
+    for (; n_ev < 9; ++n_ev)
+        if (cudaEventCreateWithFlags(&ev[n_ev], cudaEventDisableTiming) != cudaSuccess) break;
+    int rc = n_ev == 9 ? POLSAR_OK : fail(POLSAR_ECUDA, "polsar_inv_det_host: event creation failed");
+    cudaEvent_t *ev_in = ev, *ev_k = ev + 3, *ev_out = ev + 6;
     const int64_t n_chunks = (n + chunk - 1) / chunk;
     for (int64_t c = 0; c < n_chunks && rc == POLSAR_OK; ++c) {
         const int slot = (int)(c % 3);
@@ -491,8 +507,8 @@ int polsar_inv_det_host(const void* z_host, void* out_host, uint8_t* status_host
         unsigned char* dout = base + (size_t)9 * chunk * es;
         uint8_t* dst = (uint8_t*)(base + (size_t)20 * chunk * es);
         if (c >= 3) cudaStreamWaitEvent(sh, ev_out[slot], 0);  // slot drained by its D2H
-        if (cudaMemcpy2DAsync(din, chunk * es, (const unsigned char*)z_host + p0 * es, ld_host * es,
-                              m * es, 9, cudaMemcpyHostToDevice, sh) != cudaSuccess) {
+        if (!copy_planes(din, chunk * es, (const unsigned char*)z_host + p0 * es, ld_host * es, m * es, 9,
+                         cudaMemcpyHostToDevice, sh)) {
             rc = fail(POLSAR_ECUDA, "polsar_inv_det_host: H2D copy failed");
             break;
         }
@@ -503,8 +519,8 @@ int polsar_inv_det_host(const void* z_host, void* out_host, uint8_t* status_host
         if (rc != POLSAR_OK) break;
         cudaEventRecord(ev_k[slot], sc);
         cudaStreamWaitEvent(sd, ev_k[slot], 0);
-        if (cudaMemcpy2DAsync((unsigned char*)out_host + p0 * es, ld_host * es, dout, chunk * es,
-                              m * es, 11, cudaMemcpyDeviceToHost, sd) != cudaSuccess) {
+        if (!copy_planes((unsigned char*)out_host + p0 * es, ld_host * es, dout, chunk * es, m * es, 11,
+                         cudaMemcpyDeviceToHost, sd)) {
             rc = fail(POLSAR_ECUDA, "polsar_inv_det_host: D2H copy failed");
             break;
         }
@@ -515,13 +531,14 @@ int polsar_inv_det_host(const void* z_host, void* out_host, uint8_t* status_host
         }
         cudaEventRecord(ev_out[slot], sd);
     }
-    if (cudaStreamSynchronize(sd) != cudaSuccess && rc == POLSAR_OK)
-        rc = fail(POLSAR_ECUDA, "polsar_inv_det_host: stream error");
-    for (int i = 0; i < 3; ++i) {
-        cudaEventDestroy(ev_in[i]);
-        cudaEventDestroy(ev_k[i]);
-        cudaEventDestroy(ev_out[i]);
-    }
+    // Synchronous on every path: nothing this call enqueued may still read the
+    // caller's host buffers or write dev_ws after it returns, so all three
+    // streams are drained, error paths included.
+    const cudaStream_t all[3] = {sh, sc, sd};
+    for (int i = 0; i < 3; ++i)
+        if (cudaStreamSynchronize(all[i]) != cudaSuccess && rc == POLSAR_OK)
+            rc = fail(POLSAR_ECUDA, "polsar_inv_det_host: stream error");
+    for (int i = 0; i < n_ev; ++i) cudaEventDestroy(ev[i]);
     return rc;
 }
 

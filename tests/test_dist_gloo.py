@@ -20,23 +20,11 @@ def free_port():
     return p
 
 
-def _mix64(x):
-    x = np.uint64(x)
-    with np.errstate(over="ignore"):
-        x ^= x >> np.uint64(30)
-        x *= np.uint64(0xbf58476d1ce4e5b9)
-        x ^= x >> np.uint64(27)
-        x *= np.uint64(0x94d049bb133111eb)
-        x ^= x >> np.uint64(31)
-    return x
-
-
 def host_hash(vals, offset):
-    with np.errstate(over="ignore"):
-        h = np.uint64(0)
-        for p, v in enumerate(vals):
-            h += _mix64(np.uint64(v) ^ np.uint64((offset + p) * 0x9E3779B97F4A7C15 % 2**64))
-    return int(h)
+    """R1's hash of one uint32 plane (tests/_checksum_ref.py, numpy)."""
+    from tests._checksum_ref import checksum
+    v = np.asarray(vals, dtype=np.uint64).astype(np.uint32).view(np.float32)[None]
+    return checksum(v, offset)[0]
 
 
 def _worker(rank, world, port, fn, q):

@@ -39,10 +39,12 @@ def test_blocks_parity(cuda, storage, nb):
     kmax = np.max(np.stack([oracle.kappa2(zh[9 * b:9 * b + 9]) for b in range(nb)]), axis=0)
     m = kmax <= 1e4
     inv, det, idet = block_errors(out.cpu().numpy().astype(np.float64), ref, nb)
-    # det of the whole matrix: nb block dets, each within the per-block bound,
-    # multiplied with nb - 1 extra roundings
-    tol = TOL[storage] * (nb if storage == "float32" else 1)
-    assert max(inv[m].max(), det[m].max(), idet[m].max()) <= tol
+    # BASELINE's bound for every band count: K5 multiplies the block dets in
+    # the fp64 arithmetic type (nb - 1 roundings of ~1e-16) and rounds once to
+    # the storage type
+    worst = max(inv[m].max(), det[m].max(), idet[m].max())
+    print(f"[report] blocks {storage} nb={nb}: max rel err {worst:.3e}")
+    assert worst <= TOL[storage]
     assert np.all(st.cpu().numpy()[m] == 0)
 
 

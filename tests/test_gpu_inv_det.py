@@ -198,6 +198,48 @@ def test_checksum_split_invariance(c2):
     assert int(full[1]) == n
 
 
+def _u64(t):
+    return int(np.int64(t).view(np.uint64))
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_checksum_matches_numpy(c2, algo):
+    """R1 against an independent numpy evaluation of the hash definition
+    (tests/_checksum_ref.py) and a bincount of the status plane, bit-exact,
+    on the whole c2 output and on a pixel-offset slice."""
+    from tests._checksum_ref import checksum
+    z = c2[0]
+    out, st = P.inv_det(z, algo=algo)
+    n = z.shape[1]
+    res = P.polsar_checksum(out, n, 11, 0, st)
+    torch.cuda.synchronize()
+    oh, sh = out.cpu().numpy(), st.cpu().numpy()
+    h, counts = checksum(oh, 0, sh)
+    got = res.cpu().numpy()
+    assert _u64(got[0]) == h
+    assert [int(x) for x in got[1:]] == counts
+    lo, hi = 123457, 654321
+    res2 = P.polsar_checksum(out[:, lo:], hi - lo, 11, lo, st[lo:])
+    torch.cuda.synchronize()
+    h2, c2s = checksum(oh[:, lo:hi], lo, sh[lo:hi])
+    got2 = res2.cpu().numpy()
+    assert _u64(got2[0]) == h2 and [int(x) for x in got2[1:]] == c2s
+    # input planes too (9 planes, float32 bit patterns)
+    res3 = P.polsar_checksum(z, n, 9, 0)
+    torch.cuda.synchronize()
+    assert _u64(res3.cpu().numpy()[0]) == checksum(c2[1], 0)[0]
+
+
+def _host_run(z_host, algo, dt_plain, ws_bytes, status=True):
+    n = z_host.shape[1]
+    oh = torch.empty((11, z_host.stride(0)), dtype=z_host.dtype).pin_memory()[:, :n]
+    sh = torch.empty(n, dtype=torch.uint8).pin_memory() if status else None
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    P.polsar_inv_det_host(z_host, oh, sh, ws, streams, algo=algo, plain=dt_plain)
+    return oh, sh
+
+
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
 @pytest.mark.parametrize("algo", [0, 1])
 def test_host_pipeline_matches_device(c2, dt, algo):
@@ -205,14 +247,101 @@ def test_host_pipeline_matches_device(c2, dt, algo):
     n = z.shape[1]
     dev_out, dev_st = P.inv_det(z, algo="adjugate" if algo == 0 else "cholesky")
     zh = z.cpu().pin_memory()
-    oh = torch.empty((11, n), dtype=dt).pin_memory()
-    sh = torch.empty(n, dtype=torch.uint8).pin_memory()
-    ws = torch.empty(4 << 20, dtype=torch.uint8, device=z.device)  # small: many chunks
-    streams = [torch.cuda.Stream() for _ in range(3)]
-    P.polsar_inv_det_host(zh, oh, sh, ws, streams, algo=algo)
+    oh, sh = _host_run(zh, algo, False, 4 << 20)  # small workspace: many chunks
     torch.cuda.synchronize()
     assert torch.equal(oh, dev_out.cpu())
     assert torch.equal(sh, dev_st.cpu())
+
+
+@pytest.mark.parametrize("algo", [0, 1])
+def test_host_pipeline_oracle_c2(c2, algo):
+    """f-3 (PAPER.md:947-963 [§IV-C], out-of-core streaming): the chunked
+    host path against the ORACLE on all of c2 (fp32 storage), with a chunk
+    size that leaves a ragged last chunk (1048576 = 13 x 78592 + 26880)."""
+    z, zh, ref, k = c2
+    n = zh.shape[1]
+    chunk = 78592
+    ws_bytes = 3 * (20 * 4 + 1) * chunk
+    assert P.polsar_host_chunk_pixels(ws_bytes, P.POLSAR_F32) == chunk and n % chunk
+    oh, sh = _host_run(torch.from_numpy(zh).pin_memory(), algo, False, ws_bytes)
+    got = oh.numpy().astype(np.float64)
+    m = k <= 1e4
+    assert worst(got, ref, m) <= TOL["float32"]
+    exp, dec = status_expected(zh, ref, "float32")
+    assert np.array_equal(sh.numpy()[dec & m], exp[dec & m])
+
+
+@pytest.mark.parametrize("algo", [0, 1])
+def test_host_pipeline_oracle_c4_slice(cuda, algo):
+    """The chunked host path on a slice of c4 (fp64 storage, L = 8, 1 % of
+    pixels at kappa = 1e6) against the oracle at 1e-12, ragged last chunk,
+    and with a strided host view (plane stride > n)."""
+    cfg = configs.get("c4")
+    n = 250_003
+    tab = cfg.table()
+    idx = np.arange(n, dtype=np.int64) + 17 * cfg.width   # rows 17.. of the image
+    zs = wishart.generate_pixels_cpu(cfg, idx, table=tab)
+    ref = oracle.inv_det_threaded(zs, THREADS)
+    k = oracle.kappa2(zs)
+    m = k <= 1e4
+    big = torch.zeros((9, n + 1001), dtype=torch.float64).pin_memory()
+    big[:, :n] = torch.from_numpy(zs)
+    zh = big[:, :n]
+    chunk = 40_000
+    ws_bytes = 3 * (20 * 8 + 1) * chunk
+    oh, sh = _host_run(zh, algo, False, ws_bytes)
+    got = oh.numpy()
+    assert worst(got, ref, m) <= TOL["float64"]
+    exp, dec = status_expected(zs, ref, "float64")
+    assert np.array_equal(sh.numpy()[dec & m], exp[dec & m])
+    # and equal to the device path bit for bit
+    dev_out, dev_st = P.inv_det(torch.from_numpy(zs).to(cuda), algo="adjugate" if algo == 0 else "cholesky")
+    assert torch.equal(oh.contiguous(), dev_out.cpu()) and torch.equal(sh, dev_st.cpu())
+
+
+def _sparse_host_planes(nplanes, n, ld, dtype):
+    """A (nplanes, n) host view with plane stride ld over an anonymous
+    MAP_NORESERVE mapping: only the touched pages are ever backed."""
+    import mmap
+    es = torch.empty(0, dtype=dtype).element_size()
+    buf = mmap.mmap(-1, ((nplanes - 1) * ld + n) * es,
+                    flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS | 0x4000)  # 0x4000 = MAP_NORESERVE
+    return buf, torch.frombuffer(buf, dtype=dtype).as_strided((nplanes, n), (ld, 1))
+
+
+@pytest.mark.parametrize("algo", [0, 1])
+def test_host_pipeline_plane_stride_over_max_pitch(cuda, algo):
+    """2D copies cap their pitch at cudaDevAttrMaxPitch (2^31 - 1
+    bytes); a UAVSAR-scale fp64 plane stride (4e8 x 8 B) exceeds it.  Here
+    ld_host = 2^28 + 64 fp64 elements (2.1 GB pitch, pageable sparse memory):
+    the host path must copy plane by plane and still match the oracle."""
+    n, ld = 5003, (1 << 28) + 64
+    assert ld * 8 > 2 ** 31 - 1
+    try:
+        bz, zh = _sparse_host_planes(9, n, ld, torch.float64)
+        bo, oh = _sparse_host_planes(11, n, ld, torch.float64)
+    except (OSError, ValueError, OverflowError) as e:
+        pytest.skip(f"cannot map a sparse host buffer: {e}")
+    zs = wishart.generate_pixels_cpu(configs.get("c1"), np.arange(n, dtype=np.int64))
+    zh.copy_(torch.from_numpy(zs))
+    sh = torch.empty(n, dtype=torch.uint8)
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device=cuda)   # several chunks
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    P.polsar_inv_det_host(zh, oh, sh, ws, streams, algo=algo)
+    ref = oracle.inv_det(zs)
+    assert worst(oh.numpy(), ref, oracle.kappa2(zs) <= 1e4) <= TOL["float64"]
+    dev_out, dev_st = P.inv_det(torch.from_numpy(zs).to(cuda), algo="adjugate" if algo == 0 else "cholesky")
+    assert torch.equal(oh.clone(), dev_out.cpu()) and torch.equal(sh, dev_st.cpu())
+
+
+def test_host_pipeline_no_status_and_tiny(cuda):
+    """n smaller than one chunk, n = 1, and no status plane."""
+    zs = wishart.generate_pixels_cpu(configs.get("c1"), np.arange(7, dtype=np.int64))
+    ref = oracle.inv_det(zs)
+    for n in (1, 7):
+        zh = torch.from_numpy(np.ascontiguousarray(zs[:, :n])).pin_memory()
+        oh, _ = _host_run(zh, 0, False, 1 << 20, status=False)
+        assert worst(oh.numpy(), ref[:, :n], np.ones(n, bool)) <= TOL["float64"]
 
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])

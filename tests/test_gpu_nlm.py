@@ -13,8 +13,8 @@ from paper_1807_08084_b200 import configs, wishart
 pytestmark = pytest.mark.gpu
 THREADS = len(os.sched_getaffinity(0))
 # fp32 storage: BASELINE's 2e-5 (normwise over the 9 components of Zhat_i);
-# fp64: the weight error bound of test_gpu_window (4e-10)
-TOL = {torch.float32: 2e-5, torch.float64: 4e-10}
+# fp64: 1e-12 as for the window sum (SURVEY c-12; measured <= 7.2e-14)
+TOL = {torch.float32: 2e-5, torch.float64: 1e-12}
 
 
 # shapes cover the symmetric form's gather (R <= 12: several 124-column CTA
@@ -31,8 +31,9 @@ def test_nlm_parity(cuda, dt, shape, radius):
     rz, rw = oracle.nlm_threaded(zh, h, w, radius, 4.0, 1.0, np.arange(h * w), THREADS)
     got = zhat.cpu().numpy().astype(np.float64)
     err = np.max(np.abs(got - rz), axis=0) / np.max(np.abs(rz), axis=0)
-    assert err.max() <= TOL[dt], err.max()
     werr = np.abs(W.cpu().numpy() - rw) / rw
+    print(f"[report] nlm {dt} {shape} R={radius}: Zhat {err.max():.3e} W {werr.max():.3e}")
+    assert err.max() <= TOL[dt], err.max()
     assert werr.max() <= TOL[dt], werr.max()
 
 

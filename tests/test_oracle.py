@@ -406,3 +406,59 @@ def test_window_kl_constant_and_two_class():
         same = sum(1 for _ in ys for xx in xr if (xx < 5) == (x < 5))
         other = len(ys) * len(xr) - same
         assert got[p] == pytest.approx(same + other * math.exp(-dab), rel=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# The float32 entry points.  Every oracle function has a float32 loader of its
+# own (oracle/polsar_oracle.c: load_*_f32, the *_f32 wrappers and the is32
+# branch of window_kl_any).  fp32 -> binary128 / long double is exact, so a
+# float32 call must equal the float64 call on the exactly upcast inputs BIT
+# FOR BIT; the float64 entry points are pinned above.  A wrong plane index or
+# stride in a float32 loader fails here.  (PAPER.md:168-189, 390-409 [Eq. 3-5];
+# BASELINE configs[4] for the window; PAPER.md:1043-1055 [§V] for blocks.)
+# ---------------------------------------------------------------------------
+def _bits_equal(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_f32_inv_det_equals_f64_on_upcast():
+    z32 = rand_kappa(4000, 71, 1e3).astype(np.float32)
+    z32[:, :50] = rand_hpd(50, 72, scale_spread=True).astype(np.float32)
+    o32, im32 = oracle.inv_det(z32, with_imag=True)
+    o64, im64 = oracle.inv_det(z32.astype(np.float64), with_imag=True)
+    assert _bits_equal(o32, o64) and _bits_equal(im32, im64)
+
+
+@pytest.mark.parametrize("nb", [1, 2, 3])
+def test_f32_blocks_equals_f64_on_upcast(nb):
+    z32 = np.concatenate([rand_hpd(700, 80 + b).astype(np.float32) for b in range(nb)])
+    assert _bits_equal(oracle.inv_det_blocks(z32, nb),
+                       oracle.inv_det_blocks(z32.astype(np.float64), nb))
+
+
+def _window_case():
+    h, w, r = 9, 13, 3
+    z32 = rand_hpd(h * w, 91).astype(np.float32)
+    idx = np.array([0, 5, 12, 13, 40, 58, 77, h * w - 1], dtype=np.int64)
+    return z32, h, w, r, idx
+
+
+def test_f32_window_equals_f64_on_upcast():
+    z32, h, w, r, idx = _window_case()
+    for looks, hh in ((4.0, 1.0), (3.0, 0.7)):
+        assert _bits_equal(oracle.window(z32, h, w, r, looks, hh, idx),
+                           oracle.window(z32.astype(np.float64), h, w, r, looks, hh, idx))
+
+
+def test_f32_window_kl_equals_f64_on_upcast():
+    z32, h, w, r, idx = _window_case()
+    assert _bits_equal(oracle.window_kl(z32, h, w, r, 4.0, 1.0, idx),
+                       oracle.window_kl(z32.astype(np.float64), h, w, r, 4.0, 1.0, idx))
+
+
+def test_f32_nlm_equals_f64_on_upcast():
+    z32, h, w, r, idx = _window_case()
+    zh32, w32 = oracle.nlm(z32, h, w, r, 4.0, 1.0, idx)
+    zh64, w64 = oracle.nlm(z32.astype(np.float64), h, w, r, 4.0, 1.0, idx)
+    assert _bits_equal(zh32, zh64) and _bits_equal(w32, w64)
