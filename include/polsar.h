@@ -23,11 +23,17 @@
  *   Element type by `dtype`:
  *     POLSAR_F32        fp32 storage, fp64 arithmetic, each output rounded
  *                       once to fp32 (the accurate default; R-11)
- *     POLSAR_F64        fp64 storage, fp64 arithmetic with error-free
- *                       (FMA two-product / two-sum) evaluation of Alg. 2's
- *                       cofactors and determinant (R-16)
+ *     POLSAR_F64        fp64 storage, fp64 arithmetic with every cofactor
+ *                       evaluated to ~2u (FMA two-products, one exact sum)
+ *                       and a compensated Eq. 6 determinant: relative error
+ *                       ~ kappa u (<= 1e-12 at kappa <= 1e4; R-16)
  *     POLSAR_F32_PLAIN  fp32 storage and arithmetic, Alg. 2 as printed
  *     POLSAR_F64_PLAIN  fp64 storage and arithmetic, Alg. 2 as printed
+ *     POLSAR_F64_EFT    fp64 storage, error-free evaluation of Alg. 2 (the
+ *                       determinant's cofactors carried as hi + lo): a few
+ *                       ulp at any kappa, ~1.5x the FP64 work of POLSAR_F64
+ *                       (polsar_inv_det, polsar_inv_det_blocks and
+ *                       polsar_inv_det_host only; elsewhere POLSAR_ENOTSUP)
  *   The 128-bit vector path is taken when every plane base is 16-byte
  *   aligned and ld is a multiple of 16/sizeof(element); otherwise a scalar
  *   path runs the same device function and yields identical bits.
@@ -63,7 +69,8 @@ typedef enum {
     POLSAR_F32 = 0,
     POLSAR_F64 = 1,
     POLSAR_F32_PLAIN = 2,
-    POLSAR_F64_PLAIN = 3
+    POLSAR_F64_PLAIN = 3,
+    POLSAR_F64_EFT = 4
 } polsar_dtype;
 
 enum { POLSAR_OK = 0, POLSAR_EINVAL = 1, POLSAR_ECUDA = 2, POLSAR_ENOTSUP = 3 };

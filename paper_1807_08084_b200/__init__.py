@@ -10,7 +10,9 @@ Tensors: ``z`` is (9, ld) -- the packed upper triangle a, Re b, Im b, Re c,
 Im c, d, Re e, Im e, f as planes -- and ``out`` is (11, ld):
 the inverse's 9 planes, det Z, det Z^-1.  float32 tensors select POLSAR_F32
 (fp64 arithmetic) unless ``plain=True``; float64 tensors select POLSAR_F64
-(error-free-transformation Alg. 2) unless ``plain=True``.
+(Alg. 2 with ~2u cofactors and a compensated determinant) unless
+``plain=True`` (Alg. 2 as printed) or ``eft=True`` (POLSAR_F64_EFT, the
+error-free-transformation Alg. 2; inverse/det entry points only).
 """
 from __future__ import annotations
 
@@ -18,14 +20,14 @@ import ctypes
 
 from ._lib import PolsarError, check, lib
 
-POLSAR_F32, POLSAR_F64, POLSAR_F32_PLAIN, POLSAR_F64_PLAIN = 0, 1, 2, 3
+POLSAR_F32, POLSAR_F64, POLSAR_F32_PLAIN, POLSAR_F64_PLAIN, POLSAR_F64_EFT = 0, 1, 2, 3, 4
 STATUS_OK, STATUS_SINGULAR, STATUS_NOT_PD = 0, 1, 2
 
 __all__ = [
     "polsar_inv_det", "polsar_inv_det_cholesky", "polsar_inv_det_blocks", "polsar_window_distance",
     "polsar_nlm_filter", "nlm_filter", "polsar_window_kl", "window_kl", "polsar_window_workspace_bytes", "polsar_window_workspace_bytes_for", "polsar_checksum", "polsar_inv_det_host",
     "polsar_host_chunk_pixels", "inv_det", "window_distance", "dtype_code", "PolsarError",
-    "POLSAR_F32", "POLSAR_F64", "POLSAR_F32_PLAIN", "POLSAR_F64_PLAIN",
+    "POLSAR_F32", "POLSAR_F64", "POLSAR_F32_PLAIN", "POLSAR_F64_PLAIN", "POLSAR_F64_EFT",
 ]
 
 
@@ -34,12 +36,16 @@ def _torch():
     return torch
 
 
-def dtype_code(tdtype, plain: bool = False) -> int:
+def dtype_code(tdtype, plain: bool = False, eft: bool = False) -> int:
     torch = _torch()
+    if plain and eft:
+        raise ValueError("plain and eft are exclusive")
     if tdtype == torch.float32:
+        if eft:
+            raise ValueError("eft (POLSAR_F64_EFT) needs float64 storage")
         return POLSAR_F32_PLAIN if plain else POLSAR_F32
     if tdtype == torch.float64:
-        return POLSAR_F64_PLAIN if plain else POLSAR_F64
+        return POLSAR_F64_PLAIN if plain else (POLSAR_F64_EFT if eft else POLSAR_F64)
     raise TypeError(f"unsupported dtype {tdtype}")
 
 
@@ -68,7 +74,17 @@ def _planes(z, nplanes):
     return z.stride(0)
 
 
-def _inv_det_call(name, z, out, status, n, plain, stream):
+def _count(n, *tensors):
+    """Pixel count: all of z's columns by default; an explicit n must fit in
+    every tensor's pixel extent (a strided view's planes end at shape[1])."""
+    lim = min(t.shape[1] for t in tensors)
+    n = lim if n is None else int(n)
+    if n < 0 or n > lim:
+        raise ValueError(f"n = {n} outside [0, {lim}] (the tensors' pixel extent)")
+    return n
+
+
+def _inv_det_call(name, z, out, status, n, plain, stream, eft=False):
     _dev_check(z, out, status)
     ldz = _planes(z, 9)
     ldo = _planes(out, 11)
@@ -76,18 +92,18 @@ def _inv_det_call(name, z, out, status, n, plain, stream):
         raise ValueError("z and out must share the plane stride ld")
     if out.dtype != z.dtype:
         raise TypeError("z and out must have the same dtype")
-    n = z.shape[1] if n is None else int(n)
+    n = _count(n, z, out)
     if status is not None and (status.dtype != _torch().uint8 or status.numel() < n):
         raise ValueError("status must be a uint8 tensor of >= n elements")
     rc = getattr(lib(), name)(_ptr(z), _ptr(out), _ptr(status), n, ldz,
-                              dtype_code(z.dtype, plain), _stream_ptr(stream))
+                              dtype_code(z.dtype, plain, eft), _stream_ptr(stream))
     check(rc, name)
     return out
 
 
-def polsar_inv_det(z, out, status=None, n=None, plain=False, stream=None):
+def polsar_inv_det(z, out, status=None, n=None, plain=False, stream=None, eft=False):
     """Alg. 2 on every pixel: out = [Z^-1 (9), det, 1/det]."""
-    return _inv_det_call("polsar_inv_det", z, out, status, n, plain, stream)
+    return _inv_det_call("polsar_inv_det", z, out, status, n, plain, stream, eft)
 
 
 def polsar_inv_det_cholesky(z, out, status=None, n=None, plain=False, stream=None):
@@ -95,7 +111,7 @@ def polsar_inv_det_cholesky(z, out, status=None, n=None, plain=False, stream=Non
     return _inv_det_call("polsar_inv_det_cholesky", z, out, status, n, plain, stream)
 
 
-def polsar_inv_det_blocks(z, out, nblocks, status=None, n=None, plain=False, stream=None):
+def polsar_inv_det_blocks(z, out, nblocks, status=None, n=None, plain=False, stream=None, eft=False):
     """Multi-frequency block-diagonal pixels: z is
     (9*nblocks, ld), out (9*nblocks + 2, ld)."""
     _dev_check(z, out, status)
@@ -104,23 +120,27 @@ def polsar_inv_det_blocks(z, out, nblocks, status=None, n=None, plain=False, str
         raise ValueError("z and out must share the plane stride ld")
     if out.dtype != z.dtype:
         raise TypeError("z and out must have the same dtype")
-    n = z.shape[1] if n is None else int(n)
+    n = _count(n, z, out)
     if status is not None and (status.dtype != _torch().uint8 or status.numel() < n):
         raise ValueError("status must be a uint8 tensor of >= n elements")
     rc = lib().polsar_inv_det_blocks(_ptr(z), _ptr(out), _ptr(status), n, ldz, int(nblocks),
-                                     dtype_code(z.dtype, plain), _stream_ptr(stream))
+                                     dtype_code(z.dtype, plain, eft), _stream_ptr(stream))
     check(rc, "polsar_inv_det_blocks")
     return out
 
 
 def inv_det(z, algo: str = "adjugate", plain: bool = False, with_status: bool = True,
-            stream=None):
+            stream=None, eft: bool = False):
     """Allocate outputs and run K1 (algo='adjugate') or K2 (algo='cholesky')."""
     torch = _torch()
     out = torch.empty((11, z.shape[1]), dtype=z.dtype, device=z.device)
     status = torch.empty(z.shape[1], dtype=torch.uint8, device=z.device) if with_status else None
-    fn = polsar_inv_det if algo == "adjugate" else polsar_inv_det_cholesky
-    fn(z, out, status, plain=plain, stream=stream)
+    if algo == "adjugate":
+        polsar_inv_det(z, out, status, plain=plain, stream=stream, eft=eft)
+    else:
+        if eft:
+            raise ValueError("eft (POLSAR_F64_EFT) is an Alg. 2 mode")
+        polsar_inv_det_cholesky(z, out, status, plain=plain, stream=stream)
     return (out, status) if with_status else out
 
 
@@ -210,6 +230,11 @@ def polsar_nlm_filter(z, width, slab_rows, out_row_begin, out_row_end, radius, l
         raise ValueError(f"workspace needs {need} bytes")
     if out_z.dtype != z.dtype or (out_w is not None and out_w.dtype != z.dtype):
         raise TypeError("outputs must have the input dtype")
+    m = (out_row_end - out_row_begin) * width
+    if out_z.shape[1] < m or (out_w is not None and out_w.numel() < m):
+        raise ValueError(f"out_z / out_w must hold {m} pixels")
+    if z.shape[1] < slab_rows * width:
+        raise ValueError("z holds fewer than slab_rows * width pixels")
     rc = lib().polsar_nlm_filter(_ptr(z), ld, width, slab_rows, out_row_begin, out_row_end, radius,
                                  float(looks), float(h), _ptr(workspace), _ptr(out_w), _ptr(out_z),
                                  ld_out, code, _stream_ptr(stream))
@@ -252,7 +277,7 @@ def polsar_host_chunk_pixels(ws_bytes: int, dtype: int) -> int:
     return int(lib().polsar_host_chunk_pixels(ws_bytes, dtype))
 
 
-def polsar_inv_det_host(z_host, out_host, status_host, workspace, streams, algo=0, plain=False):
+def polsar_inv_det_host(z_host, out_host, status_host, workspace, streams, algo=0, plain=False, eft=False):
     """End-to-end call on HOST tensors (pinned): chunked H2D / kernel / D2H
     pipeline over three CUDA streams; returns after the last copy."""
     if z_host.is_cuda or out_host.is_cuda:
@@ -260,8 +285,10 @@ def polsar_inv_det_host(z_host, out_host, status_host, workspace, streams, algo=
     ld = _planes(z_host, 9)
     if _planes(out_host, 11) != ld:
         raise ValueError("z_host and out_host must share the plane stride")
-    n = z_host.shape[1]
-    code = dtype_code(z_host.dtype, plain)
+    n = _count(None, z_host, out_host)
+    if status_host is not None and status_host.numel() < n:
+        raise ValueError("status_host must hold >= n bytes")
+    code = dtype_code(z_host.dtype, plain, eft)
     s_h2d, s_cmp, s_d2h = (ctypes.c_void_p(s.cuda_stream) for s in streams)
     rc = lib().polsar_inv_det_host(_ptr(z_host), _ptr(out_host), _ptr(status_host), n, ld, code,
                                    int(algo), _ptr(workspace),

@@ -83,11 +83,70 @@ __device__ __forceinline__ double dot3_hi(double x1, double y1, double x2, doubl
     return __dadd_rn(r, __dadd_rn(__dadd_rn(e1, e2), t));
 }
 
+// p q - x^2 - y^2 for p q >= x^2 + y^2 (a diagonal cofactor of a positive
+// definite matrix: a principal 2x2 minor) to ~2u: as dot3_hi, but RN(p q) >=
+// RN(x^2) lets the exact sum of the first two products use FastTwoSum.
+__device__ __forceinline__ double diag_hi(double p, double q, double x, double y) {
+    double p1 = __dmul_rn(p, q), e1 = __fma_rn(p, q, -p1);
+    double p2 = __dmul_rn(x, x), e2 = __fma_rn(x, x, -p2);
+    double s = __dsub_rn(p1, p2);
+    double t = __dsub_rn(__dsub_rn(p1, s), p2);  // FastTwoSum error of p1 - p2
+    double r = __fma_rn(-y, y, s);
+    return __dadd_rn(r, __dadd_rn(__dsub_rn(e1, e2), t));
+}
+
+// Alg. 2 with every cofactor to ~2u (FMA two-products and one exact sum per
+// 3-term cofactor) and the step-2 determinant as a compensated dot over
+// (x_k, c_k): the cofactors' own ~2u errors, amplified by the row-0
+// expansion's condition (~kappa), are what is left.  Measured on c4's law
+// (tools/forms/f64_forms.py, host emulation): <= 2.5e-13 at kappa <= 1e4,
+// 6.3e-13 on matrices with kappa = 1e4 exactly; ~171 FP64 operations per
+// matrix against the error-free form's ~255, which on full-size c4 is the
+// difference between 99 % and 103 % of the HBM copy peak.  POLSAR_F64.
+__device__ __forceinline__ void alg2_comp(const H9<double>& m, double* o, double& det, double& t) {
+    // step 1 (Eq. 3)
+    const double ai = diag_hi(m.d, m.f, m.er, m.ei);
+    const double bir = dot3_hi(m.cr, m.er, m.ci, m.ei, -m.br, m.f);
+    const double bii = dot3_hi(m.ci, m.er, -m.cr, m.ei, -m.bi, m.f);
+    const double cir = dot3_hi(m.br, m.er, -m.bi, m.ei, -m.cr, m.d);
+    const double cii = dot3_hi(m.br, m.ei, m.bi, m.er, -m.ci, m.d);
+    const double di = diag_hi(m.a, m.f, m.cr, m.ci);
+    const double eir = dot3_hi(m.cr, m.br, m.ci, m.bi, -m.a, m.er);
+    const double eii = dot3_hi(m.ci, m.br, -m.cr, m.bi, -m.a, m.ei);
+    const double fi = diag_hi(m.a, m.d, m.br, m.bi);
+    // step 2 (Eq. 6), compensated
+    double p0 = __dmul_rn(m.a, ai), q0 = __fma_rn(m.a, ai, -p0);
+    double p1 = __dmul_rn(m.br, bir), q1 = __fma_rn(m.br, bir, -p1);
+    double p2 = __dmul_rn(m.bi, bii), q2 = __fma_rn(m.bi, bii, -p2);
+    double p3 = __dmul_rn(m.cr, cir), q3 = __fma_rn(m.cr, cir, -p3);
+    double p4 = __dmul_rn(m.ci, cii), q4 = __fma_rn(m.ci, cii, -p4);
+    double s, r1, r2, r3, r4;
+    two_sum(p0, p1, s, r1);
+    two_sum(s, p2, s, r2);
+    two_sum(s, p3, s, r3);
+    two_sum(s, p4, s, r4);
+    double err = __dadd_rn(__dadd_rn(__dadd_rn(q0, q1), __dadd_rn(q2, q3)),
+                           __dadd_rn(q4, __dadd_rn(__dadd_rn(r1, r2), __dadd_rn(r3, r4))));
+    det = __dadd_rn(s, err);
+    // step 3
+    t = __drcp_rn(det);
+    // step 4
+    o[0] = __dmul_rn(t, ai);
+    o[1] = __dmul_rn(t, bir);
+    o[2] = __dmul_rn(t, bii);
+    o[3] = __dmul_rn(t, cir);
+    o[4] = __dmul_rn(t, cii);
+    o[5] = __dmul_rn(t, di);
+    o[6] = __dmul_rn(t, eir);
+    o[7] = __dmul_rn(t, eii);
+    o[8] = __dmul_rn(t, fi);
+}
+
 // Alg. 2 with the five cofactors that enter Eq. 6 carried as hi + lo, the
 // other four to ~2u (dot3_hi), and the step-2 determinant summed with Dot2
 // over (x_k, hi_k) plus the x_k lo_k terms: det and every inverse entry come
 // out within a few ulp, independent of the cancellation (the plain form loses
-// ~kappa^2 u for matrices with one dominant eigenvalue).
+// ~kappa^2 u for matrices with one dominant eigenvalue).  POLSAR_F64_EFT.
 __device__ __forceinline__ void alg2_accurate(const H9<double>& m, double* o, double& det,
                                               double& t) {
     // step 1 (Eq. 3), each cofactor as a 3-term dot product
@@ -186,7 +245,7 @@ __device__ __forceinline__ bool alg1(const H9<T>& m, T* o, T& det, T& tdet) {
 // ------------------------------------------------------------------ modes
 // storage S, arithmetic per dtype code (include/polsar.h)
 enum { ALGO_ADJ = 0, ALGO_CHOL = 1 };
-enum { MATH_F64 = 0, MATH_F64_EFT = 1, MATH_F32 = 2 };
+enum { MATH_F64 = 0, MATH_F64_COMP = 1, MATH_F32 = 2, MATH_F64_EFT = 3 };
 
 template <int MATH>
 struct MathT {
@@ -213,6 +272,8 @@ __device__ __forceinline__ uint8_t solve_core(const S* in, typename MathT<MATH>:
     if constexpr (ALGO == ALGO_ADJ) {
         if constexpr (MATH == MATH_F64_EFT)
             alg2_accurate(m, o, det, t);
+        else if constexpr (MATH == MATH_F64_COMP)
+            alg2_comp(m, o, det, t);
         else
             alg2_plain<T>(m, o, det, t);
     } else {

@@ -70,7 +70,7 @@ int polsar_checksum(const void* planes, int64_t n, int64_t ld, int nplanes, int 
     if (dtype == POLSAR_F32 || dtype == POLSAR_F32_PLAIN)
         k_checksum<uint32_t><<<grid, 256, 0, s>>>((const uint32_t*)planes, n, ld, nplanes, pix_offset,
                                                   status, (unsigned long long*)result);
-    else if (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN)
+    else if (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN || dtype == POLSAR_F64_EFT)
         k_checksum<uint64_t><<<grid, 256, 0, s>>>((const uint64_t*)planes, n, ld, nplanes, pix_offset,
                                                   status, (unsigned long long*)result);
     else

@@ -138,135 +138,11 @@ k_inv_det_scalar(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restri
 }
 
 
-// ------------------------------------------------ K1 / K2, bulk-copy form
-// SURVEY §8(a) row A1, reading (ii): literally one matrix per thread, with
-// the CTA staging each plane's tile through shared memory by the bulk-copy
-// engine (cp.async.bulk, completion on an mbarrier) and writing the 11 output
-// planes + status back with bulk stores.  Persistent: one CTA of KB_THREADS
-// per SM walks tiles of TP pixels; 3 input stages and 2 output buffers keep
-// ~200 KB in flight per SM.  Selected by POLSAR_K1_VARIANT=bulk (A/B; the
-// register-vector form above is the default, DESIGN.md §6 has both numbers).
-// (mbarrier / bulk-copy helpers: common.cuh)
-constexpr int KB_THREADS = 512;
-constexpr int KB_NS = 3;  // input stages
-constexpr int KB_NO = 2;  // output buffers
-template <typename S>
-struct BulkTile {
-    static constexpr int TP = 4096 / sizeof(S);  // pixels per tile: 4 KB per plane
-};
-template <typename S>
-constexpr size_t bulk_smem_bytes() {
-    constexpr int TP = BulkTile<S>::TP;
-    return (size_t)KB_NS * 9 * TP * sizeof(S) + (size_t)KB_NO * 11 * TP * sizeof(S) + (size_t)KB_NO * TP +
-           KB_NS * sizeof(uint64_t);
-}
-
-template <typename S, int ALGO, int MATH>
-__global__ void __launch_bounds__(KB_THREADS, 1)
-k_inv_det_bulk(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
-               int64_t n_tiles, int64_t ld) {
-    constexpr int TP = BulkTile<S>::TP;
-    constexpr int PPT = TP / KB_THREADS;  // pixels per thread per tile
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    S* sin = reinterpret_cast<S*>(smem_raw);                    // [KB_NS][9][TP]
-    S* sout = sin + KB_NS * 9 * TP;                             // [KB_NO][11][TP]
-    uint8_t* sst = reinterpret_cast<uint8_t*>(sout + KB_NO * 11 * TP);  // [KB_NO][TP]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sst + KB_NO * TP);     // [KB_NS]
-    const int tid = threadIdx.x;
-    constexpr uint32_t plane_bytes = TP * sizeof(S);
-    if (tid == 0) {
-        for (int s = 0; s < KB_NS; ++s) mbar_init(&bar[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const int64_t step = gridDim.x;
-    auto issue_load = [&](int64_t t, int s) {
-        mbar_expect_tx(&bar[s], 9 * plane_bytes);
-#pragma unroll
-        for (int k = 0; k < 9; ++k)
-            bulk_g2s(sin + (s * 9 + k) * TP, z + k * ld + t * TP, plane_bytes, &bar[s]);
-    };
-    if (tid == 0)
-        for (int s = 0; s < KB_NS; ++s) {
-            const int64_t t = blockIdx.x + s * step;
-            if (t < n_tiles) issue_load(t, s);
-        }
-    int i = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += step, ++i) {
-        const int s = i % KB_NS;
-        const int ob = i % KB_NO;
-        mbar_wait(&bar[s], (uint32_t)(i / KB_NS) & 1u);
-#pragma unroll
-        for (int v = 0; v < PPT; ++v) {
-            const int q = tid + v * KB_THREADS;
-            POLSAR_CHECK(q < TP);
-            S x[9], y[11];
-            uint8_t st;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) x[k] = sin[(s * 9 + k) * TP + q];
-            solve_one<S, ALGO, MATH>(x, y, st);
-#pragma unroll
-            for (int k = 0; k < 11; ++k) sout[(ob * 11 + k) * TP + q] = y[k];
-            sst[ob * TP + q] = st;
-        }
-        // make the generic-proxy smem writes visible to the bulk (async) proxy
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
-#pragma unroll
-            for (int k = 0; k < 11; ++k) bulk_s2g(out + k * ld + t * TP, sout + (ob * 11 + k) * TP, plane_bytes);
-            if (status) bulk_s2g(status + t * TP, sst + ob * TP, TP);
-            bulk_commit();
-            const int64_t tn = t + KB_NS * step;  // stage s is free: every thread has read it
-            if (tn < n_tiles) issue_load(tn, s);
-            bulk_wait_read<KB_NO - 1>();  // the next tile's output buffer has been read out
-        }
-        __syncthreads();
-    }
-    if (tid == 0) bulk_wait<0>();
-}
-
-int k1_variant() {  // (read once; thread-safe static initialisation)
-    static const int v = [] {
-        const char* e = getenv("POLSAR_K1_VARIANT");
-        return (e && e[0] == 'b') ? 1 : 0;
-    }();
-    return v;
-}
-
-// Bulk form over the whole tiles of [0, n); returns the pixels it covers
-// (0 when the layout does not allow 16-byte bulk copies).
-template <typename S, int ALGO, int MATH>
-int64_t launch_bulk(const S* z, S* out, uint8_t* status, int64_t n, int64_t ld, cudaStream_t s) {
-    constexpr int TP = BulkTile<S>::TP;
-    const bool ok = ((uintptr_t)z % 16 == 0) && ((uintptr_t)out % 16 == 0) && ((ld * sizeof(S)) % 16 == 0) &&
-                    (status == nullptr || (uintptr_t)status % 16 == 0);
-    const int64_t n_tiles = ok ? n / TP : 0;
-    if (n_tiles == 0) return 0;
-    constexpr size_t smem = bulk_smem_bytes<S>();
-    auto kern = k_inv_det_bulk<S, ALGO, MATH>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return 0;
-        attr = true;
-    }
-    const int64_t grid = n_tiles < num_sms() ? n_tiles : num_sms();
-    kern<<<(unsigned)grid, KB_THREADS, smem, s>>>(z, out, status, n_tiles, ld);
-    return n_tiles * TP;
-}
-
 template <typename S, int ALGO, int MATH>
 int launch_inv_det(const void* zv, void* outv, uint8_t* status, int64_t n, int64_t ld,
                    cudaStream_t s) {
-    const S* z0 = (const S*)zv;
-    S* out0 = (S*)outv;
-    // optional bulk-copy form over whole tiles; the rest by the vector form
-    const int64_t nb = k1_variant() == 1 ? launch_bulk<S, ALGO, MATH>(z0, out0, status, n, ld, s) : 0;
-    const S* z = z0 + nb;
-    S* out = out0 + nb;
-    if (status) status += nb;
-    n -= nb;
+    const S* z = (const S*)zv;
+    S* out = (S*)outv;
     constexpr int W = VecSel<S, ALGO>::V::n;
     bool aligned = ((uintptr_t)z % 16 == 0) && ((uintptr_t)out % 16 == 0) && (ld % W == 0) &&
                    (status == nullptr || (uintptr_t)status % W == 0);
@@ -404,8 +280,11 @@ int dispatch_inv_det(const void* z, void* out, uint8_t* status, int64_t n, int64
     switch (dtype) {
         case POLSAR_F32: return launch_inv_det<float, ALGO, MATH_F64>(z, out, status, n, ld, s);
         case POLSAR_F64:
-            return ALGO == ALGO_ADJ ? launch_inv_det<double, ALGO, MATH_F64_EFT>(z, out, status, n, ld, s)
+            return ALGO == ALGO_ADJ ? launch_inv_det<double, ALGO, MATH_F64_COMP>(z, out, status, n, ld, s)
                                     : launch_inv_det<double, ALGO, MATH_F64>(z, out, status, n, ld, s);
+        case POLSAR_F64_EFT:
+            if constexpr (ALGO == ALGO_ADJ) return launch_inv_det<double, ALGO, MATH_F64_EFT>(z, out, status, n, ld, s);
+            return fail(POLSAR_ENOTSUP, "POLSAR_F64_EFT: Alg. 2 only");
         case POLSAR_F32_PLAIN: return launch_inv_det<float, ALGO, MATH_F32>(z, out, status, n, ld, s);
         case POLSAR_F64_PLAIN: return launch_inv_det<double, ALGO, MATH_F64>(z, out, status, n, ld, s);
         default: return fail(POLSAR_EINVAL, "bad dtype");
@@ -439,7 +318,8 @@ int polsar_inv_det_blocks(const void* z, void* out, uint8_t* status, int64_t n, 
     cudaStream_t s = (cudaStream_t)cuda_stream;
     switch (dtype) {
         case POLSAR_F32: return launch_blocks<float, MATH_F64>(z, out, status, n, ld, nblocks, s);
-        case POLSAR_F64: return launch_blocks<double, MATH_F64_EFT>(z, out, status, n, ld, nblocks, s);
+        case POLSAR_F64: return launch_blocks<double, MATH_F64_COMP>(z, out, status, n, ld, nblocks, s);
+        case POLSAR_F64_EFT: return launch_blocks<double, MATH_F64_EFT>(z, out, status, n, ld, nblocks, s);
         case POLSAR_F32_PLAIN: return launch_blocks<float, MATH_F32>(z, out, status, n, ld, nblocks, s);
         case POLSAR_F64_PLAIN: return launch_blocks<double, MATH_F64>(z, out, status, n, ld, nblocks, s);
         default: return fail(POLSAR_EINVAL, "bad dtype");
@@ -447,7 +327,7 @@ int polsar_inv_det_blocks(const void* z, void* out, uint8_t* status, int64_t n, 
 }
 
 int64_t polsar_host_chunk_pixels(size_t ws_bytes, int dtype) {
-    size_t es = (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) ? 8 : 4;
+    size_t es = (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN || dtype == POLSAR_F64_EFT) ? 8 : 4;
     // 3 slots x (9 in + 11 out planes + 1 status byte) per pixel, chunk a
     // multiple of 64 pixels so every device plane stays 256-byte aligned
     size_t per = 3 * (20 * es + 1);
@@ -463,11 +343,12 @@ int polsar_inv_det_host(const void* z_host, void* out_host, uint8_t* status_host
     if (!z_host || !out_host || !dev_ws) return fail(POLSAR_EINVAL, "null pointer");
     if ((uintptr_t)dev_ws % 256) return fail(POLSAR_EINVAL, "dev_ws must be 256-byte aligned");
     if (algo != 0 && algo != 1) return fail(POLSAR_EINVAL, "bad algo");
-    if (dtype < POLSAR_F32 || dtype > POLSAR_F64_PLAIN) return fail(POLSAR_EINVAL, "bad dtype");
+    if (dtype < POLSAR_F32 || dtype > POLSAR_F64_EFT) return fail(POLSAR_EINVAL, "bad dtype");
+    if (algo == 1 && dtype == POLSAR_F64_EFT) return fail(POLSAR_ENOTSUP, "POLSAR_F64_EFT: Alg. 2 only");
     if (!stream_h2d || !stream_compute || !stream_d2h || stream_h2d == stream_compute ||
         stream_h2d == stream_d2h || stream_compute == stream_d2h)
         return fail(POLSAR_EINVAL, "three distinct non-null streams required");
-    const size_t es = (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) ? 8 : 4;
+    const size_t es = (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN || dtype == POLSAR_F64_EFT) ? 8 : 4;
     const int64_t chunk = polsar_host_chunk_pixels(ws_bytes, dtype);
     if (chunk <= 0) return fail(POLSAR_EINVAL, "workspace too small");
     cudaStream_t sh = (cudaStream_t)stream_h2d, sc = (cudaStream_t)stream_compute,

@@ -543,6 +543,7 @@ int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_row
     if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
     if (!z || !workspace || !out_z) return fail(POLSAR_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)cuda_stream;
+    if (dtype == POLSAR_F64_EFT) return fail(POLSAR_ENOTSUP, "POLSAR_F64_EFT: inverse/det entry points only");
     // (the symmetric form's gather addresses a weight plane with 32-bit TMA coordinates)
     if (radius >= 1 && radius <= V3_RMAX && !nlm_direct() && tensor_map_encoder() &&
         slab_rows * (width + 4) + 2 * NLM_TX < ((int64_t)1 << 31)) {

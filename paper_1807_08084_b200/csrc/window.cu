@@ -113,6 +113,7 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
                                                               out, s);
             return launch_window<float, float, float>(z, ld, width, slab_rows, out_row_begin,
                                                       out_row_end, radius, looks, h, workspace, out, s);
+        case POLSAR_F64_EFT: return fail(POLSAR_ENOTSUP, "POLSAR_F64_EFT: inverse/det entry points only");
         default: return fail(POLSAR_EINVAL, "bad dtype");
     }
 }

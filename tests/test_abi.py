@@ -61,6 +61,12 @@ def test_loads_and_validates_without_gpu():
     assert b"ld" in lib.polsar_last_error()
     assert lib.polsar_inv_det(None, None, None, 0, 0, 0, None) == 0  # n == 0 no-op
     assert lib.polsar_inv_det_cholesky(None, None, None, 4, 4, 9, None) == 1
+    # POLSAR_F64_EFT (4) is an Alg. 2 mode: Alg. 1 and the window family refuse it
+    # before any CUDA call
+    dummy = ctypes.c_void_p(16)
+    assert lib.polsar_inv_det_cholesky(dummy, dummy, None, 4, 4, 4, None) == 3
+    assert b"Alg. 2" in lib.polsar_last_error()
+    assert lib.polsar_inv_det(dummy, dummy, None, 4, 4, 5, None) == 1  # unknown dtype
     assert lib.polsar_window_distance(None, 0, 4, 4, 0, 5, 11, 4.0, 1.0, None, None, 0, None) == 1
     assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 17, 4.0, 1.0, None, None, 0, None) == 1
     assert lib.polsar_window_distance(None, 16, 4, 4, 0, 4, 3, 0.0, 1.0, None, None, 0, None) == 1

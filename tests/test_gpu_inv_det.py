@@ -56,6 +56,31 @@ def test_c1_fp64_parity(c1, algo):
     assert np.all(st == 0)
 
 
+def test_c1_fp64_eft_parity(c1):
+    """POLSAR_F64_EFT (the error-free Alg. 2, R-16): a few ulp on
+    every pixel, whatever kappa -- far inside BASELINE's 1e-12."""
+    z, zh, ref, k = c1
+    out, st = P.inv_det(z, eft=True)
+    got = out.cpu().numpy()
+    assert worst(got, ref, np.isfinite(k)) <= 2e-15
+    base, _ = P.inv_det(z)
+    # the default POLSAR_F64 form and the error-free one agree within the
+    # default form's bound
+    assert worst(base.cpu().numpy(), got, k <= 1e4) <= TOL["float64"]
+
+
+def test_eft_refused_where_not_provided(c1):
+    z = c1[0]
+    with pytest.raises(ValueError):
+        P.inv_det(z, algo="cholesky", eft=True)
+    with pytest.raises(ValueError):
+        P.inv_det(z.float(), eft=True)
+    out = torch.empty((11, z.shape[1]), dtype=z.dtype, device=z.device)
+    rc = P.lib().polsar_inv_det_cholesky(P._ptr(z), P._ptr(out), None, z.shape[1], z.shape[1],
+                                         P.POLSAR_F64_EFT, None)
+    assert rc == 3  # POLSAR_ENOTSUP
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 def test_c2_fp32_parity(c2, algo):
     z, zh, ref, k = c2
@@ -342,44 +367,6 @@ def test_host_pipeline_no_status_and_tiny(cuda):
         zh = torch.from_numpy(np.ascontiguousarray(zs[:, :n])).pin_memory()
         oh, _ = _host_run(zh, 0, False, 1 << 20, status=False)
         assert worst(oh.numpy(), ref[:, :n], np.ones(n, bool)) <= TOL["float64"]
-
-
-@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
-def test_bulk_copy_variant_bit_identical(cuda, dt, tmp_path):
-    """The bulk-copy form of K1/K2 (POLSAR_K1_VARIANT=bulk, SURVEY §8(a) A1
-    reading (ii); read once per process) runs the same per-pixel arithmetic,
-    so its outputs and status equal the default form's bit for bit, across
-    whole tiles and a ragged tail handled by the vector form."""
-    import subprocess
-    import sys
-    n = 3 * 4096 + 1000 + 3
-    code = f'''
-import numpy as np, torch
-import paper_1807_08084_b200 as P
-from paper_1807_08084_b200 import configs, wishart
-z = wishart.generate(configs.get("c2").scaled(1, {n}), device="cuda").to(torch.{str(dt).split(".")[1]})
-res = {{}}
-for algo in ("adjugate", "cholesky"):
-    for plain in (False, True):
-        out, st = P.inv_det(z, algo=algo, plain=plain)
-        res[f"{{algo}}_{{plain}}"] = out.cpu().numpy()
-        res[f"{{algo}}_{{plain}}_st"] = st.cpu().numpy()
-np.savez(r"{tmp_path / 'bulk.npz'}", **res)
-print("ok")
-'''
-    env = dict(os.environ, POLSAR_K1_VARIANT="bulk")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
-                       timeout=300)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
-    got = np.load(tmp_path / "bulk.npz")
-    z = wishart.generate(configs.get("c2").scaled(1, n), device=cuda).to(dt)
-    for algo in ("adjugate", "cholesky"):
-        for plain in (False, True):
-            out, st = P.inv_det(z, algo=algo, plain=plain)
-            a, b = out.cpu().numpy(), got[f"{algo}_{plain}"]
-            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (algo, plain)
-            assert np.array_equal(st.cpu().numpy(), got[f"{algo}_{plain}_st"]), (algo, plain)
 
 
 @pytest.mark.parametrize("algo", ALGOS)

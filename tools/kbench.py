@@ -90,6 +90,17 @@ def main():
                 torch.save({"z": zz.cpu(), "w": wo.cpu()}, a.ref)
             elif ref is not None:
                 res["nlm_bit_identical_to_ref"] = bool(torch.equal(ref["z"], zz.cpu()) and torch.equal(ref["w"], wo.cpu()))
+        if "c4" in a.what:
+            c4 = configs.get("c4").scaled(a.rows)
+            z = wishart.generate(c4, device=dev, stream=s)
+            out = torch.empty((11, c4.n), dtype=z.dtype, device=dev)
+            st = torch.empty(c4.n, dtype=torch.uint8, device=dev)
+            for name, fn in (("adj", P.polsar_inv_det), ("chol", P.polsar_inv_det_cholesky)):
+                for plain in (False, True):
+                    ms = timeit(lambda: fn(z, out, st, plain=plain, stream=s), s, steps=20)
+                    key = f"{name}{'_plain' if plain else ''}_c4x{a.rows}"
+                    res[key + "_ms"] = round(ms, 4)
+                    res[key + "_pct"] = round(c4.n * 161 / ms / 1e6 / 6556.8 * 100, 1)
         if "k1" in a.what:
             c3 = configs.get("c3").scaled(a.rows)
             z = wishart.generate(c3, device=dev, stream=s)
