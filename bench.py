@@ -9,11 +9,14 @@
 A step is one pass of the hot path over one batch: the K1 kernel
 (polsar_inv_det, Alg. 2) over this rank's pixels -- inverse (9 planes),
 det Z, det Z^-1 and the status plane -- with the inputs resident in HBM.
-Default workload: BASELINE configs[2] (c3), 10000 x 40000 fp32 L=4 Wishart
-pixels per GPU (weak scaling: rank r owns rows [r*10000, (r+1)*10000) of an
-N*10000-row image; --scaling strong splits one 10000-row image instead).
+Default workload: BASELINE configs[2] (c3), one 10000 x 40000 fp32 L=4
+Wishart image whose pixel rows are sharded over the N GPUs (strong scaling,
+"pixel rows sharded over 1/2/4/8 GPUs": rank r owns rows
+[floor(r H / N), floor((r+1) H / N)); the checksum of the whole output is
+then comparable across N).  --scaling weak gives every rank 10000 rows of an
+N*10000-row image instead (its first 10000 rows are the 1-GPU image).
 Inputs (14.4 GB) and outputs (17.6 GB) are far larger than the 126 MB L2,
-so no flush is needed between steps; smaller configs flush L2 between steps.
+so no flush is needed between steps; smaller shards flush L2 between steps.
 
 Rank 0 prints one JSON line.
 """
@@ -44,7 +47,9 @@ def parse():
     p.add_argument("--config", default="c3")
     p.add_argument("--algo", choices=["adjugate", "cholesky"], default="adjugate")
     p.add_argument("--plain", action="store_true", help="Alg. as printed in storage precision")
-    p.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                   help="strong (default): one BASELINE image sharded over the GPUs; weak: a fixed "
+                        "image per GPU")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -154,11 +159,32 @@ def bytes_per_matrix(esz, status):
     return 20 * esz + (1 if status else 0)
 
 
+def workload_name(cfg, args, world):
+    base = f"{cfg.name}: BASELINE configs[{cfg.baseline_index}] {cfg.height}x{cfg.width} {cfg.dtype} L={cfg.looks}"
+    if args.scaling == "strong":
+        return base + f", the whole image sharded by pixel rows over {world} GPU(s)"
+    return base + f" per GPU (weak scaling: an image of {world}x{cfg.height} rows)"
+
+
+# The paper's own timings (Table 2): context
+# only -- another machine, precision unstated.
+PAPER_TABLE2 = {
+    "hardware": "NVIDIA GeForce 940M (3 CUs, 2 GB), OpenCL, precision unstated (PAPER.md:676-687)",
+    "replicates": 1000,
+    "simulated_5469354": {"cholesky_ms": {"t_min": 498.89, "t_avg": 507.54, "t_max": 556.79, "t_std": 9.34},
+                          "proposed_ms": {"t_min": 223.06, "t_avg": 231.51, "t_max": 273.08, "t_std": 6.11},
+                          "proposed_matrices_per_s_avg": 5469354 / 0.23151},
+    "airsar_270000": {"cholesky_ms": {"t_min": 24.68, "t_avg": 28.35, "t_max": 62.60, "t_std": 2.55},
+                      "proposed_ms": {"t_min": 11.18, "t_avg": 12.98, "t_max": 28.59, "t_std": 1.44},
+                      "proposed_matrices_per_s_avg": 270000 / 0.01298},
+    "source": "PAPER.md:875-878 (Table 2)",
+}
+
+
 def config_dict(cfg, args, world, n, H, status_plane, bpm, flushed):
     """The `config` object both arms print (same workload description)."""
     return {
-        "workload": f"{cfg.name}: BASELINE configs[{cfg.baseline_index}] "
-                    f"{cfg.height}x{cfg.width} {cfg.dtype} L={cfg.looks} per GPU",
+        "workload": workload_name(cfg, args, world),
         "algo": "Alg. 2 (adjugate)" if args.algo == "adjugate" else "Alg. 1 (Cholesky, l21 fixed)",
         "storage": cfg.dtype, "mode": "plain" if args.plain else "default",
         "pixels_per_gpu": n, "image_rows": H, "status_plane": status_plane,
@@ -169,47 +195,70 @@ def config_dict(cfg, args, world, n, H, status_plane, bpm, flushed):
 
 
 # ------------------------------------------------------------ reference arm
+def generate_host_sample(cfg, pixels, threads):
+    """The first `pixels` pixels of cfg's image from the generator's host twin
+    (bit-identical to the GPU generator), rows split over host threads."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1807_08084_b200 import wishart
+    rows = min(cfg.height, -(-pixels // cfg.width))
+    tab = cfg.table()
+    bounds = np.linspace(0, rows, max(1, min(threads, rows)) + 1).astype(int)
+    with ThreadPoolExecutor(max_workers=len(bounds) - 1) as ex:
+        parts = list(ex.map(lambda k: wishart.generate_cpu(cfg, int(bounds[k]), int(bounds[k + 1]), table=tab),
+                            range(len(bounds) - 1)))
+    return np.ascontiguousarray(np.concatenate(parts, axis=1)[:, :pixels])
+
+
 def run_reference(args):
-    """The CPU oracle (oracle/, as it stands) on the host cores, on a bounded
-    sample of the same workload per step; rank 0 only."""
+    """The CPU oracle (oracle/, as it stands: its storage-precision
+    instantiation of the cofactor definition, the -O3 -march=native build) on
+    the host cores, on a bounded sample of the same workload per step; rank 0
+    only (the other ranks exit without work)."""
     world, rank, _ = setup_dist(args)
     if rank != 0:
         return 0
     import numpy as np
 
     import oracle
-    from paper_1807_08084_b200 import configs, wishart
+    from paper_1807_08084_b200 import configs
 
     cfg = configs.get(args.config)
     if args.rows:
         cfg = cfg.scaled(args.rows)
     cores = len(os.sched_getaffinity(0))
-    sample = min(cfg.n, 1 << 22)  # 4.2M matrices per step (~0.3-0.6 s on 16 cores)
-    rows = max(1, sample // cfg.width)
-    tab = cfg.table()
-    z = wishart.generate_cpu(cfg, 0, rows, table=tab)[:, :sample].copy()
-    for _ in range(args.warmup):
-        oracle.inv_det_threaded(z, cores)
+    sample = min(cfg.n, 1 << 24)  # 16.8M matrices per step
+    z = generate_host_sample(cfg, sample, cores)
+    out = np.empty((11, sample), dtype=z.dtype)
+    for _ in range(max(args.warmup, 1)):
+        oracle.inv_det_plain(z, cores, out=out)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.inv_det_threaded(z, cores)
+        oracle.inv_det_plain(z, cores, out=out)
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
     value = sample / t
+    esz = 4 if cfg.dtype == "float32" else 8
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-        "dtype": "binary128 (oracle)", "data": "synthetic (seeded Wishart, host twin generator)",
+        "dtype": "f32" if esz == 4 else "f64",
+        "data": "synthetic (seeded Wishart, host twin generator)",
         "config": dict(config_dict(cfg, args, world, cfg.n, cfg.height * (world if args.scaling == "weak" else 1),
-                                   not args.no_status, bytes_per_matrix(4 if cfg.dtype == "float32" else 8,
-                                                                        not args.no_status), False),
+                                   not args.no_status, bytes_per_matrix(esz, not args.no_status), False),
                        sample_pixels_per_step=sample),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"first {sample} pixels of {cfg.name}, per step"},
+                         "sample": f"first {sample} pixels of {cfg.name} per step (host twin generator)",
+                         "precision": f"{'float' if esz == 4 else 'double'} (the storage precision), "
+                                      "gcc -O3 -march=native build of oracle/polsar_oracle.c",
+                         "t_step_ms": {"min": min(times) * 1e3, "avg": t * 1e3, "max": max(times) * 1e3,
+                                       "std": float(np.std(times)) * 1e3}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
+        "paper_table2_context": PAPER_TABLE2,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -327,9 +376,14 @@ def run_ours(args):
     # ---------------- side measurements (same run): K2 and K3
     if not args.no_extras and rank == 0 and world == 1:
         line["extras"] = measure_extras(args, P, torch, z, out, status, stream, dev, esz)
-    # ---------------- cpu baseline: the oracle on this host (rank 0, N=1)
-    if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = measure_cpu_baseline(z, cfg)
+    # ---------------- cpu baseline: the oracle on this host (rank 0, every N;
+    # the other ranks wait at the barrier)
+    if not args.no_cpu_baseline:
+        if rank == 0:
+            line["cpu_baseline"] = measure_cpu_baseline(z, cfg)
+        if world > 1:
+            dist.barrier()
+    line["paper_table2_context"] = PAPER_TABLE2
     if args.verify:
         line["verify"] = verify_sample(P, z, out, status, cfg, r0)
 
@@ -458,20 +512,24 @@ def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
                              "mode": "fp32 storage, L2 flushed before each launch"}
     del z2, o2, s2, flush
     torch.cuda.empty_cache()
-    # K1 on BASELINE configs[3] (c4: 4e8 px fp64 storage, error-free Alg. 2),
-    # 161 B / matrix
+    # K1 / K2 on BASELINE configs[3] (c4: 4e8 px fp64 storage), 161 B / matrix:
+    # POLSAR_F64 (Alg. 2 with ~2u cofactors, compensated Eq. 6), the
+    # error-free POLSAR_F64_EFT, and Alg. 1
     c4 = configs.get("c4")
     with torch.cuda.stream(stream):
         z4 = wishart.generate(c4, device=dev)
         o4 = torch.empty((11, c4.n), dtype=z4.dtype, device=dev)
         s4 = torch.empty(c4.n, dtype=torch.uint8, device=dev)
     stream.synchronize()
-    for algo, fn in (("adjugate", P.polsar_inv_det), ("cholesky", P.polsar_inv_det_cholesky)):
-        t = _time_kernel(torch, stream, lambda: fn(z4, o4, s4, stream=stream), max(3, steps // 2))
+    for key, fn, mode in (("c4_adjugate", lambda: P.polsar_inv_det(z4, o4, s4, stream=stream),
+                           "fp64 storage, POLSAR_F64 (compensated Alg. 2)"),
+                          ("c4_adjugate_eft", lambda: P.polsar_inv_det(z4, o4, s4, stream=stream, eft=True),
+                           "fp64 storage, POLSAR_F64_EFT (error-free Alg. 2)"),
+                          ("c4_cholesky", lambda: P.polsar_inv_det_cholesky(z4, o4, s4, stream=stream),
+                           "fp64 storage, Alg. 1")):
+        t = _time_kernel(torch, stream, fn, max(3, steps // 2))
         gbs = c4.n * 161 / t / 1e9
-        res[f"c4_{algo}"] = {"matrices_per_s": c4.n / t, "ms": t * 1e3, "GB/s": gbs,
-                             "frac_hbm": gbs / peak, "mode": "fp64 storage" +
-                             (", error-free Alg. 2" if algo == "adjugate" else "")}
+        res[key] = {"matrices_per_s": c4.n / t, "ms": t * 1e3, "GB/s": gbs, "frac_hbm": gbs / peak, "mode": mode}
     del z4, o4, s4
     torch.cuda.empty_cache()
     # K5: 3-band block-diagonal pixels of c3's law,
@@ -534,28 +592,48 @@ def window_pairs(h, w, r):
 
 
 def measure_cpu_baseline(z, cfg):
-    """The oracle (oracle/, binary128 cofactor expansion, as it stands) on
-    this box's host cores, on a bounded sample of the same workload."""
+    """SURVEY §8(d)'s CPU baseline: the oracle's storage-precision
+    instantiation of the cofactor definition (float for fp32 storage, double
+    for fp64; gcc -O3 -march=native), on this box's host cores and on one
+    core, over the first 1e7 pixels of this rank's input (D2H copy); warm-up
+    1, then 5 replicates (Table-2 style t_min / t_avg / t_max / t_std).  The
+    binary128 verification oracle's rate is reported beside it."""
+    import numpy as np
+
     import oracle
     cores = len(os.sched_getaffinity(0))
-    probe = z[:, :1 << 18].cpu().numpy()
+    m = int(min(z.shape[1], 10_000_000))
+    zs = z[:, :m].cpu().numpy()
+    out = np.empty((11, m), dtype=zs.dtype)
+
+    def reps(threads, cols, k):
+        zc = zs if cols == m else np.ascontiguousarray(zs[:, :cols])
+        o = out if cols == m else np.empty((11, cols), dtype=zs.dtype)
+        oracle.inv_det_plain(zc, threads, out=o)  # warm-up (also first-touches o)
+        ts = []
+        for _ in range(k):
+            t0 = time.perf_counter()
+            oracle.inv_det_plain(zc, threads, out=o)
+            ts.append(time.perf_counter() - t0)
+        return ts
+
+    ts = reps(cores, m, 5)
+    t = float(np.mean(ts))
+    m1 = min(m, 2_000_000)
+    ts1 = reps(1, m1, 3)
+    mq = min(m, 1 << 20)
     t0 = time.perf_counter()
-    oracle.inv_det_threaded(probe, cores)
-    rate = probe.shape[1] / (time.perf_counter() - t0)
-    sample = int(min(z.shape[1], max(1 << 20, rate * 10.0)))  # ~10 s wall on all cores
-    zs = z[:, :sample].cpu().numpy()
-    t0 = time.perf_counter()
-    oracle.inv_det_threaded(zs, cores)
-    t = time.perf_counter() - t0
-    # the same oracle on one core (SURVEY §8(d)), on a ~2 s sample
-    one = int(min(sample, max(1 << 16, rate / cores * 2.0)))
-    t1 = time.perf_counter()
-    oracle.inv_det_threaded(zs[:, :one], 1)
-    t1 = time.perf_counter() - t1
-    return {"value": sample / t, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"first {sample} pixels of this rank's {cfg.name} input (D2H copy), "
-                      f"{t:.1f} s wall on {cores} threads",
-            "single_core": {"value": one / t1, "sample": f"first {one} pixels, {t1:.1f} s on 1 thread"}}
+    oracle.inv_det_threaded(zs[:, :mq], cores)
+    tq = time.perf_counter() - t0
+    prec = "float" if zs.dtype == np.float32 else "double"
+    return {"value": m / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {m} pixels of this rank's {cfg.name} input (D2H copy), 5 replicates on "
+                      f"{cores} threads",
+            "precision": f"{prec} (the storage precision), gcc -O3 -march=native build of oracle/polsar_oracle.c",
+            "t_ms": {"min": min(ts) * 1e3, "avg": t * 1e3, "max": max(ts) * 1e3, "std": float(np.std(ts)) * 1e3},
+            "single_core": {"value": m1 / float(np.mean(ts1)), "sample": f"first {m1} pixels, 3 replicates, 1 thread"},
+            "binary128_oracle": {"value": mq / tq, "cores": cores,
+                                 "sample": f"first {mq} pixels, 1 pass (the verification oracle, not a baseline)"}}
 
 
 def verify_sample(P, z, out, status, cfg, r0):
@@ -583,10 +661,11 @@ FP64_OPS_PER_PAIR = {"window": 29, "window_mma": 20, "nlm": 40, "kl": 19}
 
 
 def run_window(args):
-    """Window kernels (BASELINE configs[4], c5) sharded by pixel rows: rank r
-    owns rows [r*2048, (r+1)*2048) of an N*2048-row image (weak scaling) and
-    its +-R halo rows are regenerated locally (exact: the generator is keyed
-    by global pixel) or exchanged with the neighbouring ranks over NCCL
+    """Window kernels (BASELINE configs[4], c5) sharded by pixel rows: the
+    2048 x 2048 image split over the N GPUs (strong, the default) or rank r
+    owning rows [r*2048, (r+1)*2048) of an N*2048-row image (weak); each
+    rank's +-R halo rows are regenerated locally (exact: the generator is
+    keyed by global pixel) or exchanged with the neighbouring ranks over NCCL
     (--halo exchange, inside the timed step)."""
     import torch
     import torch.distributed as dist
@@ -604,8 +683,10 @@ def run_window(args):
     if args.rows:
         cfg = cfg.scaled(args.rows)
     R, W = cfg.radius, cfg.width
-    H, r0, r1 = pdist.weak_rows(cfg.height, world, rank)
+    H, r0, r1 = rows_for(rank, world, cfg, args.scaling)
     s0, s1, ob, oe = pdist.halo_slab(r0, r1, H, R)
+    if args.halo == "exchange" and world > 1:
+        pdist.check_halo_geometry(r1 - r0, R, device=dev)
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
         tab = cfg.table(H)
@@ -656,7 +737,7 @@ def run_window(args):
     stream.synchronize()
     res, t_max = pdist.reduce_results(res, t_local)
     pairs_rank = window_pairs_rows(H, W, R, r0, r1)
-    pairs = pairs_rank * world
+    pairs = window_pairs_rows(H, W, R, 0, H)  # every output row of the image, over all ranks
     ops = FP64_OPS_PER_PAIR[args.kernel]
     # which form the library runs (read once per process, as the library does)
     mma = False
@@ -692,10 +773,11 @@ def run_window(args):
     line = {
         "metric": f"pairs/s ({args.kernel} search-window sum, 23x23)", "value": pairs * steps / t_max,
         "unit": "pairs/s", "n_gpus": world, "steps": steps, "warmup": max(args.warmup, 3),
-        "ms_per_step": t_max / steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t_max / steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Wishart, BASELINE law)",
-        "config": {"workload": f"c5: BASELINE configs[4] {cfg.height}x{W} float32 L={cfg.looks} "
-                               f"R={R} per GPU", "kernel": args.kernel, "halo": args.halo,
+        "config": {"workload": f"c5: BASELINE configs[4] {cfg.height}x{W} float32 L={cfg.looks} R={R}" +
+                               (f", sharded by pixel rows over {world} GPU(s)" if args.scaling == "strong"
+                                else " per GPU"), "kernel": args.kernel, "halo": args.halo,
                    "l2": "compute-bound; inputs 151 MB staged once per tile",
                    "parallelism": f"dp{world} (pixel rows + {R}-row halos)",
                    "variant": variant},

@@ -42,7 +42,35 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+def _host_tag() -> str:
+    """-march=native code is only valid on the CPU it was built for: the plain
+    build's file name carries a hash of this host's CPU model and flags (the
+    repo travels between the build container and the GPU boxes)."""
+    import hashlib
+    try:
+        with open("/proc/cpuinfo") as f:
+            lines = [l for l in f if l.startswith(("model name", "flags"))][:2]
+    except OSError:
+        lines = ["unknown"]
+    return hashlib.sha1("".join(lines).encode()).hexdigest()[:12]
+
+
+def build_plain(force: bool = False) -> str:
+    """The same source optimised for speed (-O3 -march=native, FMA contraction
+    allowed): the storage-precision entry points oracle_inv_det_plain_* are
+    SURVEY §8(d)'s plain CPU baseline.  Never used for verification."""
+    out = os.path.join(_HERE, f"liboracle_plain_{_host_tag()}.so")
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = f"{out}.{os.getpid()}.tmp"
+        cmd = ["gcc", "-O3", "-march=native", "-std=gnu11", "-fPIC", "-shared", _SRC,
+               "-o", tmp, "-lquadmath", "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(tmp, out)
+    return out
+
+
 _lib = None
+_lib_plain = None
 _lib_lock = threading.Lock()
 
 
@@ -61,8 +89,55 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
+def lib_plain() -> ctypes.CDLL:
+    global _lib_plain
+    if _lib_plain is not None:
+        return _lib_plain
+    with _lib_lock:
+        if _lib_plain is None:
+            lp = ctypes.CDLL(build_plain())
+            P, I64 = ctypes.c_void_p, ctypes.c_int64
+            lp.oracle_inv_det_plain_s.argtypes = [P, I64, P, I64, I64]
+            lp.oracle_inv_det_plain_d.argtypes = [P, I64, P, I64, I64]
+            _lib_plain = lp
+    return _lib_plain
+
+
+def inv_det_plain(z: np.ndarray, threads: int = 1, out: np.ndarray | None = None) -> np.ndarray:
+    """The cofactor definition in the storage precision (float for float32
+    input, double for float64), columns split over `threads` host threads:
+    SURVEY §8(d)'s plain CPU baseline (-O3 -march=native build).  Returns
+    (11, n) in the input dtype (into `out` when given: a reused, already
+    touched buffer keeps first-touch page faults out of a timing).  For
+    timing, not for verification."""
+    z = _planes(z)
+    n = z.shape[1]
+    if out is None:
+        out = np.empty((11, n), dtype=z.dtype)
+    if out.shape != (11, n) or out.dtype != z.dtype or not out.flags.c_contiguous:
+        raise ValueError("out must be a contiguous (11, n) array of z's dtype")
+    lp = lib_plain()
+    fn = lp.oracle_inv_det_plain_s if z.dtype == np.float32 else lp.oracle_inv_det_plain_d
+    esz = z.itemsize
+    if threads <= 1:
+        fn(_ptr(z), n, _ptr(out), n, n)
+        return out
+    bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+
+    def work(k):
+        lo, hi = int(bounds[k]), int(bounds[k + 1])
+        if hi > lo:
+            fn(_ptr(z) + lo * esz, n, _ptr(out) + lo * esz, n, hi - lo)
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(work, range(threads)))
+    return out
+
+
 def _configure(_lib: ctypes.CDLL) -> None:
     P, I64, D, INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+    _lib.oracle_inv_det_plain_s.argtypes = [P, I64, P, I64, I64]
+    _lib.oracle_inv_det_plain_d.argtypes = [P, I64, P, I64, I64]
     _lib.oracle_inv_det_f64.argtypes = [P, I64, P, I64, P, I64]
     _lib.oracle_inv_det_f32.argtypes = [P, I64, P, I64, P, I64]
     _lib.oracle_gauss_jordan.argtypes = [P, P, P]

@@ -2,7 +2,8 @@
  * polsar_oracle.c -- CPU ORACLE for arXiv 1807.08084 (TEST INFRASTRUCTURE ONLY).
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
- * reference legs may load this library.  The product path
+ * reference legs may load this library (the latter two time the storage-
+ * precision instantiation at the end of this file).  The product path
  * (paper_1807_08084_b200/) never links, imports or calls it, and this file
  * shares no code, header, table or constant with the CUDA path.
  *
@@ -482,6 +483,40 @@ void oracle_nlm_f32(const float* z, int64_t ld, int64_t height, int64_t width, i
         out[9 * m + q] = (double)acc[9];
     }
 }
+
+/* ---------------------------------------------------------------------------
+ * The same definition in the STORAGE precision: float for fp32 storage,
+ * double for fp64 -- the plain CPU implementation of SURVEY §8(d), used only
+ * as bench.py's cpu_baseline (and the --impl reference arm).  Eq. (3)
+ * cofactors, the Eq. (5) row-0 expansion (real part), Eq. (4) entrywise
+ * division and 1/det, all in type T.  bench.py times a separate
+ * -O3 -march=native build of this file (oracle.build_plain()); the accuracy
+ * oracle above stays binary128.  Pinned in tests/test_oracle.py (worked
+ * examples exactly; the binary128 oracle within kappa^2-scaled rounding).
+ * ------------------------------------------------------------------------- */
+DEFINE_HERM(float, s)
+DEFINE_HERM(double, d)
+
+#define DEFINE_PLAIN(T, SFX, IN, LOAD)                                         \
+void oracle_inv_det_plain_##SFX(const IN* z, int64_t ldz, T* out, int64_t ldo, \
+                                int64_t n) {                                   \
+    for (int64_t p = 0; p < n; ++p) {                                          \
+        herm_##SFX m = LOAD(z, ldz, p);                                        \
+        herm_##SFX c = cofactors_##SFX(m);                                     \
+        T re, im;                                                              \
+        det_full_##SFX(m, c, &re, &im);                                        \
+        out[0 * ldo + p] = c.a / re;  out[1 * ldo + p] = c.br / re;            \
+        out[2 * ldo + p] = c.bi / re; out[3 * ldo + p] = c.cr / re;            \
+        out[4 * ldo + p] = c.ci / re; out[5 * ldo + p] = c.d / re;             \
+        out[6 * ldo + p] = c.er / re; out[7 * ldo + p] = c.ei / re;            \
+        out[8 * ldo + p] = c.f / re;                                           \
+        out[9 * ldo + p] = re;                                                 \
+        out[10 * ldo + p] = (T)1 / re;                                         \
+        (void)im;                                                              \
+    }                                                                          \
+}
+DEFINE_PLAIN(float, s, float, load_s_f32)
+DEFINE_PLAIN(double, d, double, load_d_f64)
 
 /* Mantissa digits of the evaluation type, so tests can assert the oracle
  * really runs in extended precision on the host it is built on. */

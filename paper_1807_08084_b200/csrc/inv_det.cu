@@ -76,44 +76,83 @@ __device__ __forceinline__ float packv(const float* x, float*) { return x[0]; }
 
 constexpr int K1_THREADS = 128;
 
+#ifndef POLSAR_K2_MINB
+#define POLSAR_K2_MINB 1
+#endif
+#ifndef K2_U
+#define K2_U 1
+#endif
+// Vector groups per thread (compile-time A/B knob K2_U; 1 = the product):
+// U > 1 gives each thread U independent groups (ILP for Alg. 1's serial
+// DSQRT / DRCP chains) while every load and store instruction of a warp still
+// covers 32 consecutive groups: warp chunk c holds groups [32 U c, 32 U (c+1))
+// and lane l takes 32 U c + 32 j + l, j < U.  Measured on B200:
+// U = 2 or 4 and 4-pixel groups for Alg. 1 are slower than U = 1.
+template <int ALGO>
+struct GroupsPerThread {
+    static constexpr int U = ALGO == 1 ? K2_U : 1;
+};
+
 template <typename S, int ALGO, int MATH>
-__global__ void __launch_bounds__(K1_THREADS)
+__global__ void __launch_bounds__(K1_THREADS, ALGO == 1 ? POLSAR_K2_MINB : 1)
 k_inv_det_vec(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
               int64_t n_groups, int64_t ld) {
     typedef typename VecSel<S, ALGO>::V VV;
     typedef typename VV::type V;
     constexpr int W = VV::n;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_groups;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = g * W;
-        POLSAR_CHECK(p + W <= n_groups * W && p % W == 0);
-        S in[9][W];
+    constexpr int U = GroupsPerThread<ALGO>::U;
+    const int64_t n_slots = (n_groups + U - 1) / U;  // thread slots: one per U groups
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ((n_slots + 31) & ~(int64_t)31);
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g0 = (t & ~(int64_t)31) * U + (t & 31);  // this lane's first group
+        S in[U][9][W];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) unpack<V, S>(ld_stream(reinterpret_cast<const V*>(z + k * ld + p)), in[k]);
-        S res[11][W];
-        uint8_t st[W];
+        for (int j = 0; j < U; ++j) {
+            const int64_t p = (g0 + 32 * j) * W;
+            if (g0 + 32 * j < n_groups) {
 #pragma unroll
-        for (int v = 0; v < W; ++v) {
-            S x[9], y[11];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) x[k] = in[k][v];
-            solve_one<S, ALGO, MATH>(x, y, st[v]);
-#pragma unroll
-            for (int k = 0; k < 11; ++k) res[k][v] = y[k];
-        }
-#pragma unroll
-        for (int k = 0; k < 11; ++k)
-            st_stream(reinterpret_cast<V*>(out + k * ld + p), packv(res[k], (V*)nullptr));
-        if (status) {
-            if constexpr (W == 4) {
-                uint32_t w = (uint32_t)st[0] | ((uint32_t)st[1] << 8) | ((uint32_t)st[2] << 16) |
-                             ((uint32_t)st[3] << 24);
-                *reinterpret_cast<uint32_t*>(status + p) = w;
-            } else if constexpr (W == 2) {
-                uint16_t w = (uint16_t)(st[0] | (st[1] << 8));
-                *reinterpret_cast<uint16_t*>(status + p) = w;
+                for (int k = 0; k < 9; ++k)
+                    unpack<V, S>(ld_stream(reinterpret_cast<const V*>(z + k * ld + p)), in[j][k]);
             } else {
-                status[p] = st[0];
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+#pragma unroll
+                    for (int v = 0; v < W; ++v) in[j][k][v] = S(k == 0 || k == 5 || k == 8);
+            }
+        }
+        S res[U][11][W];
+        uint8_t st[U][W];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+#pragma unroll
+            for (int v = 0; v < W; ++v) {
+                S x[9], y[11];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) x[k] = in[j][k][v];
+                solve_one<S, ALGO, MATH>(x, y, st[j][v]);
+#pragma unroll
+                for (int k = 0; k < 11; ++k) res[j][k][v] = y[k];
+            }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t g = g0 + 32 * j;
+            if (g >= n_groups) continue;
+            const int64_t p = g * W;
+            POLSAR_CHECK(p + W <= n_groups * W && p % W == 0);
+#pragma unroll
+            for (int k = 0; k < 11; ++k)
+                st_stream(reinterpret_cast<V*>(out + k * ld + p), packv(res[j][k], (V*)nullptr));
+            if (status) {
+                if constexpr (W == 4) {
+                    uint32_t w = (uint32_t)st[j][0] | ((uint32_t)st[j][1] << 8) | ((uint32_t)st[j][2] << 16) |
+                                 ((uint32_t)st[j][3] << 24);
+                    *reinterpret_cast<uint32_t*>(status + p) = w;
+                } else if constexpr (W == 2) {
+                    uint16_t w = (uint16_t)(st[j][0] | (st[j][1] << 8));
+                    *reinterpret_cast<uint16_t*>(status + p) = w;
+                } else {
+                    status[p] = st[j][0];
+                }
             }
         }
     }
@@ -149,7 +188,9 @@ int launch_inv_det(const void* zv, void* outv, uint8_t* status, int64_t n, int64
     int64_t n_vec = aligned ? (n / W) * W : 0;
     if (n_vec > 0) {
         int64_t groups = n_vec / W;
-        k_inv_det_vec<S, ALGO, MATH><<<grid_full(groups, K1_THREADS), K1_THREADS, 0, s>>>(z, out, status, groups, ld);
+        constexpr int U = GroupsPerThread<ALGO>::U;
+        const int64_t slots = ((groups + U - 1) / U + 31) & ~(int64_t)31;
+        k_inv_det_vec<S, ALGO, MATH><<<grid_full(slots, K1_THREADS), K1_THREADS, 0, s>>>(z, out, status, groups, ld);
     }
     if (n > n_vec) {
         k_inv_det_scalar<S, ALGO, MATH>

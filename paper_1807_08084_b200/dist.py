@@ -37,12 +37,32 @@ def halo_slab(r0: int, r1: int, height: int, radius: int):
     return s0, s1, r0 - s0, r1 - s0
 
 
+def check_halo_geometry(own_rows: int, radius: int, device=None, group=None):
+    """Collective check (all ranks, MIN-reduced) that every rank owns at least
+    `radius` rows: then each halo comes from the adjacent rank alone and the
+    rows a rank sends equal the rows its neighbour expects.  Raises
+    ValueError on every rank otherwise (instead of a mismatched send/recv
+    that could hang).  Call once before ``exchange_halos``."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([own_rows], dtype=torch.int64, device=device)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    if int(t.item()) < radius:
+        raise ValueError(f"halo exchange needs every rank to own >= R = {radius} rows "
+                         f"(smallest shard: {int(t.item())}); use local regeneration")
+
+
 def exchange_halos(slab, width: int, own_begin: int, own_end: int, radius: int, group=None):
     """Fill the halo rows of `slab` (a (planes, rows*width) tensor holding the
     rank's slab rows, own rows at [own_begin, own_end)) from the neighbouring
     ranks with point-to-point send/recv (NCCL on GPU, gloo on CPU).  Each
     rank sends its first/last `radius` own rows to rank-1 / rank+1.  Slab
-    geometry must come from ``halo_slab`` on every rank."""
+    geometry must come from ``halo_slab`` on every rank, and every rank must
+    own >= radius rows (``check_halo_geometry``): then a rank's top and bottom
+    halos are exactly `radius` rows wherever it has a neighbour, so the rows
+    sent and the rows received match on both sides."""
     import torch.distributed as dist
 
     rank = dist.get_rank(group)
@@ -50,6 +70,9 @@ def exchange_halos(slab, width: int, own_begin: int, own_end: int, radius: int, 
     ops = []
     top = own_begin                       # halo rows above our own rows
     bot = slab.shape[1] // width - own_end  # halo rows below
+    if own_end - own_begin < radius or (rank > 0 and top != radius) or (rank < world - 1 and bot != radius):
+        raise ValueError("exchange_halos: every rank must own >= R rows with R-row halos towards "
+                         "its neighbours (check_halo_geometry)")
     if rank > 0 and top > 0:
         send = slab[:, own_begin * width:(own_begin + top) * width].contiguous()
         recv = slab[:, :top * width]

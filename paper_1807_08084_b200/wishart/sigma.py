@@ -31,21 +31,28 @@ def _cn(rng, shape):
 
 
 def cholesky_table(sig: np.ndarray) -> np.ndarray:
-    """(n, 3, 3) Hermitian PD -> (n, 9) lower Cholesky factors (elementwise)."""
+    """(n, 3, 3) Hermitian PD -> (n, 9) lower Cholesky factors (elementwise).
+
+    Real arithmetic only: numpy's complex division and multiplication take
+    different SIMD / tail paths by array length, so a row's factor could
+    depend on how many rows the table has; real ufuncs are one correctly
+    rounded IEEE operation per element, whatever the length."""
     sig = np.asarray(sig, dtype=np.complex128).reshape(-1, 3, 3)
     s00, s11, s22 = sig[:, 0, 0].real, sig[:, 1, 1].real, sig[:, 2, 2].real
-    s10, s20, s21 = sig[:, 1, 0], sig[:, 2, 0], sig[:, 2, 1]
+    s10r, s10i = sig[:, 1, 0].real, sig[:, 1, 0].imag
+    s20r, s20i = sig[:, 2, 0].real, sig[:, 2, 0].imag
+    s21r, s21i = sig[:, 2, 1].real, sig[:, 2, 1].imag
     c00 = np.sqrt(s00)
-    c10 = s10 / c00
-    c20 = s20 / c00
-    c11 = np.sqrt(s11 - (c10.real * c10.real + c10.imag * c10.imag))
-    c21 = (s21 - c20 * np.conj(c10)) / c11
-    c22 = np.sqrt(s22 - (c20.real * c20.real + c20.imag * c20.imag)
-                  - (c21.real * c21.real + c21.imag * c21.imag))
+    c10r, c10i = s10r / c00, s10i / c00
+    c20r, c20i = s20r / c00, s20i / c00
+    c11 = np.sqrt(s11 - (c10r * c10r + c10i * c10i))
+    # c21 = (s21 - c20 conj(c10)) / c11
+    c21r = (s21r - (c20r * c10r + c20i * c10i)) / c11
+    c21i = (s21i - (c20i * c10r - c20r * c10i)) / c11
+    c22 = np.sqrt(s22 - (c20r * c20r + c20i * c20i) - (c21r * c21r + c21i * c21i))
     if not (np.all(np.isfinite(c11)) and np.all(np.isfinite(c22)) and np.all(c22 > 0)):
         raise ValueError("Sigma is not positive definite")
-    return np.stack([c00, c10.real, c10.imag, c11, c20.real, c20.imag, c21.real, c21.imag, c22],
-                    axis=1).astype(np.float64)
+    return np.stack([c00, c10r, c10i, c11, c20r, c20i, c21r, c21i, c22], axis=1).astype(np.float64)
 
 
 def sigma_from_table(tab: np.ndarray) -> np.ndarray:
@@ -82,11 +89,25 @@ def haar_unitary(n: int, rng) -> np.ndarray:
     return q
 
 
+PER_ROW_BLOCK = 1024
+
+
 def per_row(rows: int, seed: int, stream: int, kappa_max: float = 1e3) -> np.ndarray:
-    """Sigma_r = U diag(1, k^u, k) U^H for r < rows (configs[2], [3])."""
-    rng = _rng(seed, stream, 2)
-    u_haar = haar_unitary(rows, rng)
-    kap = np.exp(rng.uniform(0.0, 1.0, rows) * np.log(kappa_max))
-    u = rng.uniform(0.0, 1.0, rows)
-    lam = np.stack([np.ones(rows), kap ** u, kap], axis=1)
-    return (u_haar * lam[:, None, :]) @ np.conj(np.transpose(u_haar, (0, 2, 1)))
+    """Sigma_r = U diag(1, k^u, k) U^H for r < rows (configs[2], [3]).
+
+    Prefix-stable: rows are drawn in blocks of PER_ROW_BLOCK, block b from its
+    own PCG64 stream keyed by (seed, stream id, tag, b), so row r's Sigma
+    depends only on (seed, stream, r) -- per_row(h)[:m] == per_row(m) for any
+    m <= h.  An N-GPU image of N x H rows (weak scaling) therefore starts with
+    the 1-GPU image, and a pixel's input never depends on the image height."""
+    blocks = []
+    for b in range((rows + PER_ROW_BLOCK - 1) // PER_ROW_BLOCK):
+        rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, stream, 2, b])))
+        u_haar = haar_unitary(PER_ROW_BLOCK, rng)
+        kap = np.exp(rng.uniform(0.0, 1.0, PER_ROW_BLOCK) * np.log(kappa_max))
+        u = rng.uniform(0.0, 1.0, PER_ROW_BLOCK)
+        lam = np.stack([np.ones(PER_ROW_BLOCK), kap ** u, kap], axis=1)
+        blocks.append((u_haar * lam[:, None, :]) @ np.conj(np.transpose(u_haar, (0, 2, 1))))
+    if not blocks:
+        return np.zeros((0, 3, 3), dtype=np.complex128)
+    return np.concatenate(blocks)[:rows]

@@ -44,3 +44,23 @@ def test_full_image_halves(bench):
     h, w, r = 40, 33, 11
     n = h * w
     assert bench.unordered_pairs_rows(h, w, r, 0, h) * 2 == bench.window_pairs_rows(h, w, r, 0, h) - n
+
+
+def test_default_is_the_whole_baseline_image(bench, monkeypatch):
+    """bench.py's default N > 1 line measures BASELINE configs[2] itself: one
+    10000 x 40000 image whose pixel rows are split over the ranks (strong
+    scaling), so the union of the shards is the 1-GPU image and the output
+    checksum is comparable across N."""
+    import sys
+    from paper_1807_08084_b200 import configs
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "8"])
+    args = bench.parse()
+    assert args.scaling == "strong" and args.config == "c3"
+    cfg = configs.get("c3")
+    rows = []
+    for rank in range(8):
+        H, r0, r1 = bench.rows_for(rank, 8, cfg, args.scaling)
+        assert H == cfg.height
+        rows.extend(range(r0, r1))
+    assert rows == list(range(cfg.height))
+    assert "whole image sharded" in bench.workload_name(cfg, args, 8)

@@ -98,6 +98,45 @@ def test_halo_exchange_gloo_3ranks():
     assert all(res.values())
 
 
+def _small_shard_job(rank, world):
+    """H = 7 rows over 3 ranks at R = 3: rank 0 owns 2 rows < R.  Every rank
+    must refuse (ValueError from the collective check), none may hang."""
+    H, W, R = 7, 4, 3
+    r0, r1 = pdist.shard_rows(H, world, rank)
+    try:
+        pdist.check_halo_geometry(r1 - r0, R)
+    except ValueError:
+        return "refused"
+    return "accepted"
+
+
+def test_halo_exchange_refuses_small_shards():
+    res = spawn(_small_shard_job, 3)
+    assert set(res.values()) == {"refused"}
+
+
+def _rows_job(rank, world):
+    """The rows a rank generates (host twin of the generator) equal the same
+    rows of the 1-GPU image, under both sharding modes of bench.py: strong
+    (one configs[2]-law image split) and weak (an N-times taller image whose
+    first rows are the 1-GPU image; the per-row Sigma table is prefix-stable)."""
+    from paper_1807_08084_b200 import configs, wishart
+    cfg = configs.get("c3").scaled(40, 64)
+    one = wishart.generate_cpu(cfg, 0, cfg.height, table=cfg.table())
+    r0, r1 = pdist.shard_rows(cfg.height, world, rank)
+    strong = wishart.generate_cpu(cfg, r0, r1, table=cfg.table())
+    ok_strong = np.array_equal(strong, one[:, r0 * cfg.width:r1 * cfg.width])
+    H, w0, w1 = pdist.weak_rows(cfg.height, world, rank)
+    weak = wishart.generate_cpu(cfg, w0, w1, table=cfg.table(H), height=H)
+    ok_weak = rank != 0 or np.array_equal(weak, one)
+    return bool(ok_strong and ok_weak)
+
+
+def test_rank_rows_equal_single_gpu_image():
+    res = spawn(_rows_job, 2)
+    assert all(res.values())
+
+
 def _reduce_job(rank, world):
     vals = (np.arange(1000, dtype=np.uint64) * np.uint64(2654435761)) % np.uint64(2**32)
     r0, r1 = pdist.shard_rows(len(vals), world, rank)

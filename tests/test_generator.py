@@ -33,6 +33,17 @@ def test_cholesky_tables_reconstruct_sigma():
         np.testing.assert_allclose(S.sigma_from_table(tab), sig, rtol=1e-13, atol=1e-13)
 
 
+def test_per_row_prefix_stable():
+    """Row r's Sigma depends only on (seed, stream, r): the table of a taller
+    image starts with the shorter image's table (weak-scaling images of N x H
+    rows start with the 1-GPU image)."""
+    a = S.per_row(2500, 0, 3)
+    for m in (1, 1023, 1024, 1025, 2048):
+        assert np.array_equal(S.per_row(m, 0, 3), a[:m])
+    c3 = configs.get("c3")
+    assert np.array_equal(c3.table(20000)[:c3.height], c3.table())
+
+
 def test_per_row_condition_numbers():
     sig = S.per_row(2000, 0, 3)
     w = np.linalg.eigvalsh(sig)

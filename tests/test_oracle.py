@@ -462,3 +462,43 @@ def test_f32_nlm_equals_f64_on_upcast():
     zh32, w32 = oracle.nlm(z32, h, w, r, 4.0, 1.0, idx)
     zh64, w64 = oracle.nlm(z32.astype(np.float64), h, w, r, 4.0, 1.0, idx)
     assert _bits_equal(zh32, zh64) and _bits_equal(w32, w64)
+
+
+# ---------------------------------------------------------------------------
+# The storage-precision instantiation (oracle_inv_det_plain_s / _d, SURVEY
+# §8(d)'s plain CPU baseline; timed by bench.py, built -O3 -march=native).
+# Pinned to the worked examples (exact for the dyadic ones) and to the
+# binary128 definition within the rounding error of the cofactor expansion,
+# which grows like kappa^2 u (R-16): a dropped term, wrong sign or
+# transposed operand gives O(1) errors and fails.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("row", parse_golden(), ids=lambda r: r[0])
+def test_plain_worked_examples(dt, row):
+    name, zin, inv, det, idet = row
+    out = oracle.inv_det_plain(zin.reshape(9, 1).astype(dt), 1)
+    assert out.dtype == dt
+    u = np.finfo(dt).eps
+    if name in ("identity", "diag245", "golden"):
+        assert np.array_equal(out[:9, 0], inv.astype(dt))
+        assert out[9, 0] == det and out[10, 0] == dt(idet)
+    else:
+        np.testing.assert_allclose(out[:9, 0], inv, rtol=0, atol=8 * u * np.abs(inv).max())
+        assert out[9, 0] == pytest.approx(det, rel=8 * u)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("threads", [1, 3])
+def test_plain_against_binary128(dt, threads):
+    z = np.concatenate([rand_hpd(3000, 11), rand_kappa(3000, 12, 1e2)], axis=1).astype(dt)
+    ref = oracle.inv_det(z)
+    got = oracle.inv_det_plain(z, threads).astype(np.float64)
+    k = oracle.kappa2(z)
+    u = float(np.finfo(dt).eps) / 2
+    inv = normwise(got[:9], ref[:9])
+    det = np.abs(got[9] - ref[9]) / np.abs(ref[9])
+    idet = np.abs(got[10] - ref[10]) / np.abs(ref[10])
+    bound = 32 * k ** 2 * u
+    assert np.all(inv <= bound) and np.all(det <= bound) and np.all(idet <= bound + 2 * u)
+    # and it is the storage-precision evaluation, not a wider one
+    assert inv.max() > u / 4
