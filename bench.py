@@ -566,15 +566,12 @@ def measure_extras(args, P, torch, z, out, status, stream, dev, esz):
         res[f"window_c5{'_plain' if plain else ''}"] = {
             "pairs_per_s": pairs / t, "ms": t * 1e3, "pairs": pairs,
             "mode": "fp32 storage, fp32 weight, " + ("fp32 pair det" if plain else "fp64 pair det") +
-                    ("" if plain or os.environ.get("POLSAR_WINDOW_MMA", "") == "0"
-                     else " (DMMA mixed-discriminant pass 1)")}
+                    ("" if plain else " (DMMA mixed-discriminant pass 1)")}
     # K6 (KL window) and K4 (NLM filter) on the same c5 input
     t = _time_kernel(torch, stream, lambda: P.polsar_window_kl(
         z5, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, w5, stream=stream), steps)
     res["kl_window_c5"] = {"pairs_per_s": pairs / t, "ms": t * 1e3, "pairs": pairs,
-                           "mode": "symmetric Wishart KL, fp32 storage, fp64 trace products" +
-                                   ("" if os.environ.get("POLSAR_WINDOW_MMA", "") == "0"
-                                    else " (DMMA pass 1)")}
+                           "mode": "symmetric Wishart KL, fp32 storage, fp64 trace products (DMMA pass 1)"}
     zn = torch.empty((9, c5.n), dtype=z5.dtype, device=dev)
     t = _time_kernel(torch, stream, lambda: P.polsar_nlm_filter(
         z5, c5.width, c5.height, 0, c5.height, c5.radius, c5.looks, c5.h, ws, zn, w5, stream=stream), steps)
@@ -739,23 +736,19 @@ def run_window(args):
     pairs_rank = window_pairs_rows(H, W, R, r0, r1)
     pairs = window_pairs_rows(H, W, R, 0, H)  # every output row of the image, over all ranks
     ops = FP64_OPS_PER_PAIR[args.kernel]
-    # which form the library runs (read once per process, as the library does)
+    # which form the library runs (fixed at compile time: csrc/window.cu, nlm.cu)
     mma = False
     if args.kernel == "nlm":
-        symmetric = not os.environ.get("POLSAR_NLM_VARIANT", "").startswith("d") and R <= 12
-        variant = "symmetric two-pass (pass 1 + TMA gather)" if symmetric else "direct"
+        symmetric = 1 <= R <= 12
+        variant = ("symmetric two-pass (pass 1 + TMA gather, 512-row bands)" if symmetric else "direct")
     else:
-        v = os.environ.get("POLSAR_WINDOW_VARIANT", "4")
-        symmetric = v not in ("2", "3") and R <= 12
-        variant = "symmetric two-pass" if symmetric else {"3": "det expansion", "2": "direct"}.get(v, v)
-        if args.kernel == "kl" and not symmetric:
-            variant = "streaming expansion"
-        # the tensor-core pass 1 (csrc/window_mma.cuh; default for the fp32-storage log-det
-        # window): each unordered pair is a 20-term fp64 dot product, 20 FMAs on the same
-        # FP64 datapath (DMMA.8x8x4 shares the 64 FMA/clk/SM peak)
-        # (the KL window's too: its two trace products and the -6 are the same 20-term product)
-        mma = (symmetric and os.environ.get("POLSAR_WINDOW_MMA", "") != "0"
-               and os.environ.get("POLSAR_WINDOW_PLANES", "") != "1" and cfg.dtype == "float32")
+        symmetric = R <= 12
+        variant = "symmetric two-pass" if symmetric else "direct"
+        # the tensor-core pass 1 (csrc/window_mma.cuh; the product for fp32 storage): each
+        # unordered pair is a 20-term fp64 dot product, 20 FMAs on the same FP64 datapath
+        # (DMMA.8x8x4 shares the 64 FMA/clk/SM peak); the KL window's two trace
+        # products and the -6 are the same 20-term product
+        mma = symmetric and cfg.dtype == "float32"
         if mma:
             variant = "symmetric two-pass, pass 1 on the FP64 tensor cores (DMMA)"
             ops = FP64_OPS_PER_PAIR["window_mma"]

@@ -544,25 +544,40 @@ int polsar_nlm_filter(const void* z, int64_t ld, int64_t width, int64_t slab_row
     if (!z || !workspace || !out_z) return fail(POLSAR_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)cuda_stream;
     if (dtype == POLSAR_F64_EFT) return fail(POLSAR_ENOTSUP, "POLSAR_F64_EFT: inverse/det entry points only");
-    // (the symmetric form's gather addresses a weight plane with 32-bit TMA coordinates)
-    if (radius >= 1 && radius <= V3_RMAX && !nlm_direct() && tensor_map_encoder() &&
-        slab_rows * (width + 4) + 2 * NLM_TX < ((int64_t)1 << 31)) {
-        switch (dtype) {
-            case POLSAR_F32:
-                return launch_nlm_sym<float, double, float>(z, ld, width, slab_rows, out_row_begin,
-                                                            out_row_end, radius, looks, h, workspace,
-                                                            out_w, out_z, ld_out, s);
-            case POLSAR_F64:
-            case POLSAR_F64_PLAIN:
-                return launch_nlm_sym<double, double, double>(z, ld, width, slab_rows, out_row_begin,
-                                                              out_row_end, radius, looks, h, workspace,
-                                                              out_w, out_z, ld_out, s);
-            case POLSAR_F32_PLAIN:
-                return launch_nlm_sym<float, float, float>(z, ld, width, slab_rows, out_row_begin,
-                                                           out_row_end, radius, looks, h, workspace,
-                                                           out_w, out_z, ld_out, s);
-            default: return fail(POLSAR_EINVAL, "bad dtype");
+    // the symmetric form, band by band (NLM_BAND output rows, each band a
+    // sub-slab with its R-row halos; the workspace covers one band); its
+    // gather addresses a weight plane with 32-bit TMA coordinates
+    const int64_t band_rows = nlm_band_slab_rows(slab_rows, radius);
+    if (nlm_sym_ok(radius) && tensor_map_encoder() &&
+        band_rows * (width + 4) + 2 * NLM_TX < ((int64_t)1 << 31)) {
+        const size_t es = (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) ? 8 : 4;
+        for (int64_t b0 = out_row_begin; b0 < out_row_end; b0 += NLM_BAND) {
+            const int64_t b1 = b0 + NLM_BAND < out_row_end ? b0 + NLM_BAND : out_row_end;
+            const int64_t s0 = b0 - radius > 0 ? b0 - radius : 0;
+            const int64_t s1 = b1 + radius < slab_rows ? b1 + radius : slab_rows;
+            const void* zb = (const unsigned char*)z + (size_t)(s0 * width) * es;
+            void* wb = out_w ? (void*)((unsigned char*)out_w + (size_t)((b0 - out_row_begin) * width) * es) : nullptr;
+            void* ob = (unsigned char*)out_z + (size_t)((b0 - out_row_begin) * width) * es;
+            int rc;
+            switch (dtype) {
+                case POLSAR_F32:
+                    rc = launch_nlm_sym<float, double, float>(zb, ld, width, s1 - s0, b0 - s0, b1 - s0, radius, looks,
+                                                              h, workspace, wb, ob, ld_out, s);
+                    break;
+                case POLSAR_F64:
+                case POLSAR_F64_PLAIN:
+                    rc = launch_nlm_sym<double, double, double>(zb, ld, width, s1 - s0, b0 - s0, b1 - s0, radius,
+                                                                looks, h, workspace, wb, ob, ld_out, s);
+                    break;
+                case POLSAR_F32_PLAIN:
+                    rc = launch_nlm_sym<float, float, float>(zb, ld, width, s1 - s0, b0 - s0, b1 - s0, radius, looks,
+                                                             h, workspace, wb, ob, ld_out, s);
+                    break;
+                default: return fail(POLSAR_EINVAL, "bad dtype");
+            }
+            if (rc != POLSAR_OK) return rc;
         }
+        return POLSAR_OK;
     }
     switch (dtype) {
         case POLSAR_F32:

@@ -16,47 +16,29 @@ extern "C" {
 size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t width, int radius,
                                          int dtype) {
     if (!slab_size_ok(slab_rows, width) || radius < 0 || entry < 0 || entry > 2) return 0;
+    if (dtype != POLSAR_F32 && dtype != POLSAR_F64 && dtype != POLSAR_F32_PLAIN && dtype != POLSAR_F64_PLAIN)
+        return 0;
     const int64_t n = slab_rows * width;
     const bool wt64 = dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN;
     const size_t wt = wt64 ? 8 : 4;
     auto up = [](size_t b) { return (b + 255) / 256 * 256; };
     const bool sym_ok = radius <= V3_RMAX;
-    const int v = window_variant();
-    // the largest need of the kernels this entry point may run (with this
-    // process's POLSAR_* A/B settings, which the library reads the same way)
-    size_t b = up((size_t)n * wt);  // direct forms: one plane of g
-    if (entry == 0) {                // polsar_window_distance
-        if (sym_ok && v == 3 && dtype != POLSAR_F32_PLAIN) b = std::max(b, up((size_t)n * 160));
-        if (use_window_mma(dtype, radius))
-            b = std::max(b, mma_sym_bytes(slab_rows, width, radius));
-        if (sym_ok && v == 4) {
-            b = std::max(b, acc_sym_bytes((size_t)n * wt, slab_rows, width, radius, POLSAR_SYM_TY));
-            if (window_planes())
-                b = std::max(b, wt64 ? window_sym_bytes<double>(slab_rows, width, radius)
-                                     : window_sym_bytes<float>(slab_rows, width, radius));
-        }
-    } else if (entry == 1) {         // polsar_nlm_filter (the dispatch conditions of the gather form)
-        if (sym_ok && radius >= 1 && !nlm_direct() && slab_rows * (width + 4) + 2 * NLM_TX < ((int64_t)1 << 31))
-            b = std::max(b, wt64 ? window_sym_bytes<double>(slab_rows, width, radius)
-                                 : window_sym_bytes<float>(slab_rows, width, radius));
-    } else {                         // polsar_window_kl (radius <= 12; no fp32-arithmetic mode)
-        if (dtype == POLSAR_F32_PLAIN || !sym_ok) return 0;
-        if (use_window_mma(dtype, radius))  // the tensor-core form: F | tile sums only
-            return std::max(b, mma_sym_bytes(slab_rows, width, radius));
-        b = std::max(b, up((size_t)n * 160));  // prepass planes (the streaming form's too)
-        if (v == 4) {  // the choice of launch_window_kl_sym
-            const size_t pre = (size_t)n * V3_NP * sizeof(double);
-            const bool planes = window_planes();
-            if (!wt64 && !planes && acc_fwd_smem<KLPairF<float>>(POLSAR_KLF_TY, radius) <= K3_SMEM_MAX)
-                b = std::max(b, acc_sym_bytes(pre, slab_rows, width, radius, POLSAR_KLF_TY));
-            else if (!planes && acc_fwd_smem<KLPair<float>>(16, radius) <= K3_SMEM_MAX)
-                b = std::max(b, acc_sym_bytes(pre, slab_rows, width, radius, 16));
-            else  // the weight-plane form (POLSAR_WINDOW_PLANES=1, or R = 12)
-                b = std::max(b, wt64 ? kl_sym_bytes<double>(slab_rows, width, radius)
-                                     : kl_sym_bytes<float>(slab_rows, width, radius));
-        }
+    // the need of the form this entry point runs for (dtype, radius) -- the
+    // dispatch below, fixed at compile time (no environment switches)
+    if (entry == 0) {  // polsar_window_distance
+        if (!sym_ok) return up((size_t)n * wt);  // the direct form: one plane of g
+        if (use_window_mma(dtype, radius)) return mma_sym_bytes(slab_rows, width, radius);
+        return window_sym_need(dtype, slab_rows, width, radius);
     }
-    return b;
+    if (entry == 1) {  // polsar_nlm_filter
+        if (!nlm_sym_ok(radius)) return up((size_t)n * wt);
+        const int64_t rows = nlm_band_slab_rows(slab_rows, radius);
+        return wt64 ? window_sym_bytes<double>(rows, width, radius) : window_sym_bytes<float>(rows, width, radius);
+    }
+    // polsar_window_kl (radius <= 12; no fp32-arithmetic mode)
+    if (dtype == POLSAR_F32_PLAIN || !sym_ok) return 0;
+    if (use_window_mma(dtype, radius)) return mma_sym_bytes(slab_rows, width, radius);
+    return kl_sym_need(dtype, slab_rows, width, radius);
 }
 
 size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radius, int dtype) {
@@ -84,35 +66,25 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
                                                      looks, h, workspace, out, s)
                    : launch_window_mma<double, double>(z, ld, width, slab_rows, out_row_begin, out_row_end,
                                                        radius, looks, h, workspace, out, s);
+    // the symmetric two-pass form for R <= V3_RMAX, else the direct form
+    const bool sym = radius <= V3_RMAX;
     switch (dtype) {
         case POLSAR_F32:
-            if (radius <= V3_RMAX && window_variant() == 3)
-                return launch_window_v3<float, float>(z, ld, width, slab_rows, out_row_begin,
-                                                      out_row_end, radius, looks, h, workspace, out, s);
-            if (radius <= V3_RMAX && window_variant() == 4)
-                return launch_window_sym<float, double, float>(z, ld, width, slab_rows, out_row_begin,
-                                                               out_row_end, radius, looks, h, workspace,
-                                                               out, s);
-            return launch_window<float, double, float>(z, ld, width, slab_rows, out_row_begin,
-                                                       out_row_end, radius, looks, h, workspace, out, s);
+            return sym ? launch_window_sym<float, double, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                                 radius, looks, h, workspace, out, s)
+                       : launch_window<float, double, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                             radius, looks, h, workspace, out, s);
         case POLSAR_F64:
         case POLSAR_F64_PLAIN:
-            if (radius <= V3_RMAX && window_variant() == 3)
-                return launch_window_v3<double, double>(z, ld, width, slab_rows, out_row_begin,
-                                                        out_row_end, radius, looks, h, workspace, out, s);
-            if (radius <= V3_RMAX && window_variant() == 4)
-                return launch_window_sym<double, double, double>(z, ld, width, slab_rows, out_row_begin,
-                                                                 out_row_end, radius, looks, h,
-                                                                 workspace, out, s);
-            return launch_window<double, double, double>(z, ld, width, slab_rows, out_row_begin,
-                                                         out_row_end, radius, looks, h, workspace, out, s);
+            return sym ? launch_window_sym<double, double, double>(z, ld, width, slab_rows, out_row_begin,
+                                                                   out_row_end, radius, looks, h, workspace, out, s)
+                       : launch_window<double, double, double>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                               radius, looks, h, workspace, out, s);
         case POLSAR_F32_PLAIN:
-            if (radius <= V3_RMAX && window_variant() == 4)
-                return launch_window_sym<float, float, float>(z, ld, width, slab_rows, out_row_begin,
-                                                              out_row_end, radius, looks, h, workspace,
-                                                              out, s);
-            return launch_window<float, float, float>(z, ld, width, slab_rows, out_row_begin,
-                                                      out_row_end, radius, looks, h, workspace, out, s);
+            return sym ? launch_window_sym<float, float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                                radius, looks, h, workspace, out, s)
+                       : launch_window<float, float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                            radius, looks, h, workspace, out, s);
         case POLSAR_F64_EFT: return fail(POLSAR_ENOTSUP, "POLSAR_F64_EFT: inverse/det entry points only");
         default: return fail(POLSAR_EINVAL, "bad dtype");
     }
@@ -138,19 +110,13 @@ int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows
                                                           radius, looks, h, workspace, out, s);
     switch (dtype) {
         case POLSAR_F32:
-            if (window_variant() == 4)
-                return launch_window_kl_sym<float, float>(z, ld, width, slab_rows, out_row_begin,
-                                                          out_row_end, radius, looks, h, workspace, out, s);
-            return launch_window_kl<float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end,
-                                                  radius, looks, h, workspace, out, s);
+            return launch_window_kl_sym<float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end, radius,
+                                                      looks, h, workspace, out, s);
         case POLSAR_F64:
         case POLSAR_F64_PLAIN:
-            if (window_variant() == 4)
-                return launch_window_kl_sym<double, double>(z, ld, width, slab_rows, out_row_begin,
-                                                            out_row_end, radius, looks, h, workspace,
-                                                            out, s);
-            return launch_window_kl<double, double>(z, ld, width, slab_rows, out_row_begin,
-                                                    out_row_end, radius, looks, h, workspace, out, s);
+            return launch_window_kl_sym<double, double>(z, ld, width, slab_rows, out_row_begin, out_row_end,
+                                                        radius, looks, h, workspace, out, s);
+        case POLSAR_F64_EFT: return fail(POLSAR_ENOTSUP, "POLSAR_F64_EFT: inverse/det entry points only");
         default: return fail(POLSAR_ENOTSUP, "polsar_window_kl: fp32-arithmetic mode not provided");
     }
 }

@@ -322,36 +322,10 @@ int launch_window(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, 
 }
 
 // ------------------------------------------------------------------------
-// K3 (v3, the fp64-determinant modes): the pair determinant by the 3x3
-// expansion  det(A + B) = det A + det B + <adj A, B> + <A, adj B>,
-// <X, Y> = tr(X Y) = sum_k w_k x_k y_k over the packed components with
-// w = (1, 2, 2, 2, 2, 1, 2, 2, 1).  Alg. 2's cofactors (Eq. 3) and
-// determinant (Eq. 6) are evaluated ONCE per pixel in the prepass; each pair
-// then costs one add and 18 FMAs instead of 9 adds and 20 multiply-adds
-// (S = Z_i + Z_j, then Eq. 6 on S).  All four terms are >= 0 for positive-
-// definite pixels, so the sum itself cannot cancel.
-//
-// Prepass (K3a v3) writes 20 fp64 planes per slab pixel:
-//   0..8   z   (the packed Z)
-//   9..17  u = w * adj(Z) (cofactors a_c, b_c, c_c, d_c, e_c, f_c, weighted)
-//   18     D = det Z (Eq. 6)
-//   19     g = 1 / (8 D) as float in the low 4 bytes
-// Main pass (K3b v3): a CTA owns a 256-column x RB-row output block (each
-// thread one column, RB rows).  The window rows it needs stream through
-// shared memory V3_CH rows at a time (all 20 planes, 256 + 2R' columns),
-// double-buffered with cp.async so the next rows load while the current ones
-// are consumed.  Every thread of the CTA pairs each staged row with the same
-// owned rows, so the per-row work is identical across warps (no barrier
-// imbalance), and each staged Z_j serves RB pairs.
-constexpr int V3_TX = 256;
-constexpr int V3_RB = 4;
-constexpr int V3_CH = 2;
-constexpr int V3_NP = 20;        // planes per pixel
-constexpr int V3_THREADS = V3_TX;
-constexpr int V3_RMAX = 12;      // radius limit of this kernel (the paper's R = 11)
-constexpr int V3_XOFF = V3_RMAX; // column of x0 inside a staged row (even)
-constexpr int V3_SW = V3_TX + 2 * V3_XOFF;  // staged row width (compile-time strides)
-constexpr int V3_CHP = V3_CH * V3_SW;       // pixels per chunk plane
+// Shared by the symmetric forms: the largest radius whose tiles fit shared
+// memory (the paper's R = 11) and the KL prepass's plane count.
+constexpr int V3_NP = 20;        // prepass planes per pixel (KL: Z | w Z^-1 | 0 | 0)
+constexpr int V3_RMAX = 12;      // radius limit of the symmetric and tensor-core forms
 
 // KL prepass: planes 9..17 hold w * Z^-1 from Alg. 2
 // (K1's device function: cofactors, Eq. 6 det, t = 1/det, scale), plane 18
@@ -388,51 +362,6 @@ k_window_prep_kl(const S* __restrict__ z, int64_t ld, int64_t n, double* __restr
     }
 }
 
-template <typename S, typename WT>
-__global__ void __launch_bounds__(256)
-k_window_prep_v3(const S* __restrict__ z, int64_t ld, int64_t n, double* __restrict__ ws) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        H9<double> m;
-        m.a = (double)z[0 * ld + p];
-        m.br = (double)z[1 * ld + p];
-        m.bi = (double)z[2 * ld + p];
-        m.cr = (double)z[3 * ld + p];
-        m.ci = (double)z[4 * ld + p];
-        m.d = (double)z[5 * ld + p];
-        m.er = (double)z[6 * ld + p];
-        m.ei = (double)z[7 * ld + p];
-        m.f = (double)z[8 * ld + p];
-        // Eq. 3 cofactors (Alg. 2 step 1) and Eq. 6 determinant (step 2)
-        double ac = FMA(m.d, m.f, -FMA(m.er, m.er, MUL(m.ei, m.ei)));
-        double bcr = FMA(m.cr, m.er, FMA(m.ci, m.ei, -MUL(m.br, m.f)));
-        double bci = FMA(m.ci, m.er, -FMA(m.cr, m.ei, MUL(m.bi, m.f)));
-        double ccr = FMA(m.br, m.er, -FMA(m.bi, m.ei, MUL(m.cr, m.d)));
-        double cci = FMA(m.br, m.ei, FMA(m.bi, m.er, -MUL(m.ci, m.d)));
-        double dc = FMA(m.a, m.f, -FMA(m.cr, m.cr, MUL(m.ci, m.ci)));
-        double ecr = FMA(m.cr, m.br, FMA(m.ci, m.bi, -MUL(m.a, m.er)));
-        double eci = FMA(m.ci, m.br, -FMA(m.cr, m.bi, MUL(m.a, m.ei)));
-        double fc = FMA(m.a, m.d, -FMA(m.br, m.br, MUL(m.bi, m.bi)));
-        double det = FMA(m.a, ac, FMA(m.br, bcr, FMA(m.bi, bci, FMA(m.cr, ccr, MUL(m.ci, cci)))));
-        const int64_t P = n;  // plane stride of the workspace
-        ws[0 * P + p] = m.a;  ws[1 * P + p] = m.br; ws[2 * P + p] = m.bi;
-        ws[3 * P + p] = m.cr; ws[4 * P + p] = m.ci; ws[5 * P + p] = m.d;
-        ws[6 * P + p] = m.er; ws[7 * P + p] = m.ei; ws[8 * P + p] = m.f;
-        ws[9 * P + p] = ac;
-        ws[10 * P + p] = 2.0 * bcr; ws[11 * P + p] = 2.0 * bci;
-        ws[12 * P + p] = 2.0 * ccr; ws[13 * P + p] = 2.0 * cci;
-        ws[14 * P + p] = dc;
-        ws[15 * P + p] = 2.0 * ecr; ws[16 * P + p] = 2.0 * eci;
-        ws[17 * P + p] = fc;
-        ws[18 * P + p] = det;
-        const double g = 1.0 / (8.0 * det);
-        if constexpr (std::is_same<WT, float>::value)
-            ws[19 * P + p] = __longlong_as_double((long long)(unsigned)__float_as_uint((float)g));
-        else
-            ws[19 * P + p] = g;
-    }
-}
-
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
     unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     int src_bytes = valid ? 8 : 0;  // 0: zero-fill
@@ -444,15 +373,6 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
 // plane 19 holds g as fp64 (fp64 weights) or as fp32 bits in the low word
-template <typename WT>
-__device__ __forceinline__ WT load_g(double v);
-template <>
-__device__ __forceinline__ float load_g<float>(double v) {
-    return __uint_as_float((unsigned)__double_as_longlong(v));
-}
-template <>
-__device__ __forceinline__ double load_g<double>(double v) { return v; }
-
 // Weight of a pair for the symmetric Wishart KL distance:
 // T = tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i), d = L (T/2 - 3), w = exp(-d/h);
 // lk = L/h.  The subtraction is done in fp64 (T/2 ~ 3 for similar pixels).
@@ -466,273 +386,6 @@ __device__ __forceinline__ float weight_kl<float>(double T, float lk) {
 template <>
 __device__ __forceinline__ double weight_kl<double>(double T, double lk) {
     return exp(-lk * __fma_rn(T, 0.5, -3.0));
-}
-
-template <typename WT>
-__device__ __forceinline__ WT weight_v3(double T, WT gi, WT gj, WT alpha, bool a2) {
-    WT ft = (WT)T;
-    WT rr = (ft * gi) * (ft * gj);
-    return pair_weight(rr, alpha, a2);
-}
-
-// one pair: T = det(Z_i + Z_j) = D_i + D_j + <u_i, z_j> + <z_i, u_j>
-__device__ __forceinline__ double pair_T(const double* ui, const double* zi, double Di,
-                                         const double* uj, const double* zj, double Dj) {
-    double a = __fma_rn(ui[0], zj[0], __dadd_rn(Di, Dj));
-    double b = __dmul_rn(ui[6], zj[6]);
-    double c = __dmul_rn(zi[3], uj[3]);
-    a = __fma_rn(ui[1], zj[1], a);
-    b = __fma_rn(ui[7], zj[7], b);
-    c = __fma_rn(zi[4], uj[4], c);
-    a = __fma_rn(ui[2], zj[2], a);
-    b = __fma_rn(ui[8], zj[8], b);
-    c = __fma_rn(zi[5], uj[5], c);
-    a = __fma_rn(ui[3], zj[3], a);
-    b = __fma_rn(zi[0], uj[0], b);
-    c = __fma_rn(zi[6], uj[6], c);
-    a = __fma_rn(ui[4], zj[4], a);
-    b = __fma_rn(zi[1], uj[1], b);
-    c = __fma_rn(zi[7], uj[7], c);
-    a = __fma_rn(ui[5], zj[5], a);
-    b = __fma_rn(zi[2], uj[2], b);
-    c = __fma_rn(zi[8], uj[8], c);
-    return __dadd_rn(a, __dadd_rn(b, c));
-}
-
-
-// T_r = det(Z_{i_r} + Z_j) for the RB owned pixels at once, written as
-// 2*RB independent FMA chains (k-outer, pixel-inner) so the FP64 pipe always
-// has independent work in flight.
-template <int RB>
-__device__ __forceinline__ void pair_T_block(const double (&ui)[RB][9], const double (&zi)[RB][9],
-                                             const double (&Di)[RB], const double* uj,
-                                             const double* zj, double Dj, double (&T)[RB]) {
-    double A[RB], B[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        A[r] = __fma_rn(ui[r][0], zj[0], Di[r]);
-        B[r] = __fma_rn(zi[r][0], uj[0], Dj);
-    }
-#pragma unroll
-    for (int k = 1; k < 9; ++k) {
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            A[r] = __fma_rn(ui[r][k], zj[k], A[r]);
-            B[r] = __fma_rn(zi[r][k], uj[k], B[r]);
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r) T[r] = __dadd_rn(A[r], B[r]);
-}
-
-enum { DIST_LOGDET = 0, DIST_KL = 1 };
-
-template <int KIND, typename WT>
-__device__ __forceinline__ WT weight_kind(double T, WT gi, WT gj, WT alpha, bool a2) {
-    if constexpr (KIND == DIST_KL)
-        return weight_kl<WT>(T, alpha);
-    else
-        return weight_v3<WT>(T, gi, gj, alpha, a2);
-}
-
-template <typename S, typename WT, bool A2, int KIND = DIST_LOGDET>
-__global__ void __launch_bounds__(V3_THREADS, 1)
-k_window_sum_v3(const double* __restrict__ ws, int64_t width, int64_t slab_rows, int64_t row_begin,
-                int64_t row_end, int R, double alpha_d, S* __restrict__ out) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int XOFF = V3_XOFF, SW = V3_SW, CHP = V3_CHP;
-    double* buf = reinterpret_cast<double*>(smem_raw);  // [2][V3_NP][V3_CH][SW]
-    const int64_t P = slab_rows * width;                // workspace plane stride
-
-    const int64_t x0 = (int64_t)blockIdx.x * V3_TX;
-    const int64_t y0 = row_begin + (int64_t)blockIdx.y * V3_RB;
-    // window rows of the block, clipped to the slab
-    const int64_t ja = y0 - R > 0 ? y0 - R : 0;
-    const int64_t jb = (y0 + V3_RB - 1 + R) < slab_rows - 1 ? (y0 + V3_RB - 1 + R) : slab_rows - 1;
-    const int nrows = (int)(jb - ja + 1);
-    const int nchunks = (nrows + V3_CH - 1) / V3_CH;
-
-    auto load_chunk = [&](int c, int b) {
-        double* dst = buf + (size_t)b * V3_NP * CHP;
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        for (int pr = warp; pr < V3_NP * V3_CH; pr += V3_THREADS / 32) {
-            const int pl = pr / V3_CH, row = pr % V3_CH;  // compile-time divisors
-            const int64_t gy = ja + (int64_t)c * V3_CH + row;
-            const bool rok = gy <= jb;
-            const double* srow = ws + pl * P + (rok ? gy : 0) * width;
-            double* drow = dst + pl * CHP + row * SW;
-            for (int col = lane; col < SW; col += 32) {
-                POLSAR_CHECK(pl * CHP + row * SW + col < V3_NP * CHP);
-                const int64_t gxx = x0 - XOFF + col;
-                const bool ok = rok && gxx >= 0 && gxx < width;
-                cp_async8(drow + col, srow + (ok ? gxx : 0), ok);
-            }
-        }
-        cp_async_commit();
-    };
-    load_chunk(0, 0);
-
-    // owned pixels: column gx, rows y0 .. y0 + RB - 1
-    const int tx = threadIdx.x;
-    const int64_t gx = x0 + tx;
-    double ui[V3_RB][9], zi[V3_RB][9], Di[V3_RB];
-    WT gi[V3_RB];
-    double acc[V3_RB];
-#pragma unroll
-    for (int r = 0; r < V3_RB; ++r) {
-        const int64_t gy = y0 + r;
-        const bool ok = gx < width && gy < slab_rows;
-        const int64_t p = ok ? gy * width + gx : 0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            zi[r][k] = ok ? ws[k * P + p] : 0.0;
-            ui[r][k] = ok ? ws[(9 + k) * P + p] : 0.0;
-        }
-        Di[r] = ok ? ws[18 * P + p] : 0.0;
-        gi[r] = ok ? load_g<WT>(ws[19 * P + p]) : WT(0);
-        acc[r] = 0.0;
-    }
-    const WT alpha = (WT)alpha_d;
-    constexpr bool a2 = A2;
-    const bool interior_x = (x0 - R >= 0) && (x0 + V3_TX + R <= width);
-
-    for (int c = 0; c < nchunks; ++c) {
-        if (c + 1 < nchunks) {
-            load_chunk(c + 1, (c + 1) & 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const double* cb = buf + (size_t)(c & 1) * V3_NP * CHP;
-#pragma unroll 1
-        for (int row = 0; row < V3_CH; ++row) {
-            const int64_t gyj = ja + (int64_t)c * V3_CH + row;
-            if (gyj > jb) break;
-            const int dy0 = (int)(gyj - y0);  // dy of owned row r is dy0 - r (CTA-uniform)
-            const double* rb = cb + row * SW + XOFF + tx;
-            WT rowacc[V3_RB];
-#pragma unroll
-            for (int r = 0; r < V3_RB; ++r) rowacc[r] = WT(0);
-            const bool all = (dy0 - (V3_RB - 1) >= -R) && (dy0 <= R);
-            if (all) {
-                // software-pipelined: the weights of column wx-1 (F2F / FMUL /
-                // MUFU, long-latency) are evaluated alongside the FMA chains of
-                // column wx, so the FP64 pipe never waits on the weight tail
-                double Tp[V3_RB];
-                WT gp = WT(0);
-                bool okp = false;
-#pragma unroll
-                for (int r = 0; r < V3_RB; ++r) Tp[r] = 1.0;
-#pragma unroll 1
-                for (int wx = -R; wx <= R; ++wx) {
-                    double zj[9], uj[9];
-                    POLSAR_CHECK(row * SW + XOFF + tx + wx >= 0 && row * SW + XOFF + tx + wx < CHP);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) {
-                        zj[k] = rb[k * CHP + wx];
-                        uj[k] = rb[(9 + k) * CHP + wx];
-                    }
-                    const double Dj = rb[18 * CHP + wx];
-                    const WT gj = load_g<WT>(rb[19 * CHP + wx]);
-                    const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-                    double T[V3_RB];
-                    pair_T_block<V3_RB>(ui, zi, Di, uj, zj, Dj, T);
-#pragma unroll
-                    for (int r = 0; r < V3_RB; ++r) {
-                        WT w = weight_kind<KIND, WT>(Tp[r], gi[r], gp, alpha, a2);
-                        rowacc[r] += okp ? w : WT(0);
-                        Tp[r] = T[r];
-                    }
-                    gp = gj;
-                    okp = colok;
-                }
-#pragma unroll
-                for (int r = 0; r < V3_RB; ++r) {
-                    WT w = weight_kind<KIND, WT>(Tp[r], gi[r], gp, alpha, a2);
-                    rowacc[r] += okp ? w : WT(0);
-                }
-            } else {
-#pragma unroll 1
-                for (int wx = -R; wx <= R; ++wx) {
-                    double zj[9], uj[9];
-                    POLSAR_CHECK(row * SW + XOFF + tx + wx >= 0 && row * SW + XOFF + tx + wx < CHP);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) {
-                        zj[k] = rb[k * CHP + wx];
-                        uj[k] = rb[(9 + k) * CHP + wx];
-                    }
-                    const double Dj = rb[18 * CHP + wx];
-                    const WT gj = load_g<WT>(rb[19 * CHP + wx]);
-                    const bool colok = interior_x || (gx + wx >= 0 && gx + wx < width);
-#pragma unroll
-                    for (int r = 0; r < V3_RB; ++r) {
-                        const int dy = dy0 - r;
-                        if (dy >= -R && dy <= R) {  // CTA-uniform
-                            WT w = weight_kind<KIND, WT>(pair_T(ui[r], zi[r], Di[r], uj, zj, Dj), gi[r], gj, alpha, a2);
-                            rowacc[r] += colok ? w : WT(0);
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < V3_RB; ++r) acc[r] += (double)rowacc[r];
-        }
-        __syncthreads();  // buffer (c & 1) is refilled by the prefetch of chunk c + 2
-    }
-#pragma unroll
-    for (int r = 0; r < V3_RB; ++r) {
-        const int64_t gy = y0 + r;
-        if (gx < width && gy < row_end) out[(gy - row_begin) * width + gx] = (S)acc[r];
-    }
-}
-
-template <typename S, typename WT>
-int launch_window_v3(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                     int64_t re, int R, double looks, double h, void* wsv, void* outv,
-                     cudaStream_t s) {
-    const int64_t n = slab_rows * width;
-    double* ws = (double*)wsv;
-    k_window_prep_v3<S, WT><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, ws);
-    size_t smem = (size_t)2 * V3_NP * V3_CHP * sizeof(double);
-    const double alpha = looks / (2.0 * h);
-    auto kern = alpha == 2.0 ? k_window_sum_v3<S, WT, true> : k_window_sum_v3<S, WT, false>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_window_distance: shared memory request too large");
-    dim3 grid((unsigned)((width + V3_TX - 1) / V3_TX), (unsigned)((re - rb + V3_RB - 1) / V3_RB));
-    kern<<<grid, V3_THREADS, smem, s>>>(ws, width, slab_rows, rb, re, R, alpha, (S*)outv);
-    return launch_check("polsar_window_distance: launch failed");
-}
-
-template <typename S, typename WT>
-int launch_window_kl(const void* zv, int64_t ld, int64_t width, int64_t slab_rows, int64_t rb,
-                     int64_t re, int R, double looks, double h, void* wsv, void* outv,
-                     cudaStream_t s) {
-    const int64_t n = slab_rows * width;
-    double* ws = (double*)wsv;
-    k_window_prep_kl<S><<<grid_for(n, 256), 256, 0, s>>>((const S*)zv, ld, n, ws);
-    size_t smem = (size_t)2 * V3_NP * V3_CHP * sizeof(double);
-    auto kern = k_window_sum_v3<S, WT, false, DIST_KL>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return fail(POLSAR_ENOTSUP, "polsar_window_kl: shared memory request too large");
-    dim3 grid((unsigned)((width + V3_TX - 1) / V3_TX), (unsigned)((re - rb + V3_RB - 1) / V3_RB));
-    kern<<<grid, V3_THREADS, smem, s>>>(ws, width, slab_rows, rb, re, R, looks / h, (S*)outv);
-    return launch_check("polsar_window_kl: launch failed");
-}
-
-// Window kernel variant (R <= 12): 4 (symmetric two-pass, default), 2 (direct
-// Eq. 6 on S = Z_i + Z_j for every ordered pair), 3 (cubic expansion over
-// per-pixel adjugates).  POLSAR_WINDOW_VARIANT=2|3 selects the alternatives
-// for A/B runs; all are parity-tested.  R > 12 always runs variant 2.
-// (read once; function-local static initialisation is thread-safe)
-int window_variant() {
-    static const int v = [] {
-        const char* e = getenv("POLSAR_WINDOW_VARIANT");
-        return (e && (e[0] == '2' || e[0] == '3')) ? e[0] - '0' : 4;
-    }();
-    return v;
 }
 
 // ------------------------------------------------------------------------
@@ -1350,15 +1003,13 @@ inline size_t acc_sym_bytes(size_t pre_bytes, int64_t slab_rows, int64_t width, 
            up((size_t)fg.nbx * fg.nby * fg.HP * sizeof(long long));
 }
 
-// Window / KL symmetric form: backward sums in shared memory (ACC, default)
-// or through the weight planes (POLSAR_WINDOW_PLANES=1, the A/B alternative).
-bool window_planes() {
-    static const bool v = [] {
-        const char* e = getenv("POLSAR_WINDOW_PLANES");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
+// Compile-time A/B switch (tools/build_variant.sh -DPOLSAR_WINDOW_PLANES=1;
+// the product never reads the environment): route the window sums through
+// the weight-plane form even where the shared-memory backward sums fit.
+#ifndef POLSAR_WINDOW_PLANES
+#define POLSAR_WINDOW_PLANES 0
+#endif
+constexpr bool window_planes() { return POLSAR_WINDOW_PLANES != 0; }
 
 template <typename S, typename WT>
 void launch_bwd(const WT* wbuf, const double* fbuf, int64_t width, int64_t slab_rows, int64_t rb,
@@ -1470,19 +1121,65 @@ int launch_window_kl_sym(const void* zv, int64_t ld, int64_t width, int64_t slab
     return launch_check("polsar_window_kl: launch failed");
 }
 
+// NLM form: symmetric (pass 1 + gather, the product for 1 <= R <= V3_RMAX) or
+// the direct form (always for R = 0 and R > V3_RMAX; compile-time A/B switch
+// -DPOLSAR_NLM_DIRECT=1 for every radius).
+#ifndef POLSAR_NLM_DIRECT
+#define POLSAR_NLM_DIRECT 0
+#endif
+constexpr bool nlm_direct() { return POLSAR_NLM_DIRECT != 0; }
+
 // The NLM gather's CTA width (threads = TMA tile length); here because the
 // workspace query applies the gather's dispatch conditions.
 constexpr int NLM_TX = 128;
 
-// NLM variant: symmetric (pass 1 + gather, default for R <= V3_RMAX) or the
-// direct form (POLSAR_NLM_VARIANT=direct, and always for R > V3_RMAX).
-bool nlm_direct() {
-    static const bool v = [] {
-        const char* e = getenv("POLSAR_NLM_VARIANT");
-        return e && e[0] == 'd';
-    }();
-    return v;
+// Workspace of launch_window_sym / launch_window_kl_sym for (dtype, R): the
+// same form choice those launchers make.
+template <typename S, typename T, typename WT>
+size_t window_sym_need_t(int64_t slab_rows, int64_t width, int R) {
+    if (!window_planes() && acc_fwd_smem<LogDetPair<S, T, WT, 1>>(POLSAR_SYM_TY, R) <= K3_SMEM_MAX)
+        return acc_sym_bytes((size_t)slab_rows * width * sizeof(WT), slab_rows, width, R, POLSAR_SYM_TY);
+    return window_sym_bytes<WT>(slab_rows, width, R);
 }
+inline size_t window_sym_need(int dtype, int64_t slab_rows, int64_t width, int R) {
+    switch (dtype) {
+        case POLSAR_F32: return window_sym_need_t<float, double, float>(slab_rows, width, R);
+        case POLSAR_F32_PLAIN: return window_sym_need_t<float, float, float>(slab_rows, width, R);
+        default: return window_sym_need_t<double, double, double>(slab_rows, width, R);
+    }
+}
+inline size_t kl_sym_need(int dtype, int64_t slab_rows, int64_t width, int R) {
+    const size_t pre = (size_t)slab_rows * width * V3_NP * sizeof(double);
+    if (dtype == POLSAR_F32) {
+        if (!window_planes() && acc_fwd_smem<KLPairF<float>>(POLSAR_KLF_TY, R) <= K3_SMEM_MAX)
+            return acc_sym_bytes(pre, slab_rows, width, R, POLSAR_KLF_TY);
+        if (!window_planes() && acc_fwd_smem<KLPair<float>>(16, R) <= K3_SMEM_MAX)
+            return acc_sym_bytes(pre, slab_rows, width, R, 16);
+        return kl_sym_bytes<float>(slab_rows, width, R);
+    }
+    if (!window_planes() && acc_fwd_smem<KLPair<double>>(16, R) <= K3_SMEM_MAX)
+        return acc_sym_bytes(pre, slab_rows, width, R, 16);
+    return kl_sym_bytes<double>(slab_rows, width, R);
+}
+
+// NLM bands.  The symmetric NLM keeps every forward weight of its slab in
+// weight planes (2R(R+1) values per pixel: 1.07 KB at R = 11 in fp32), so
+// polsar_nlm_filter walks the output rows in bands of at most NLM_BAND rows,
+// each band a sub-slab with its own R-row halos (the slab decomposition is
+// bit-exact): the workspace covers one band's sub-slab, not
+// the image -- ~2.3 GB at a 2048-pixel width, ~46 GB for a 40000-pixel-wide
+// UAVSAR image of any height -- at the cost of recomputing R halo rows of
+// forward weights per band (1 % at R = 11) and one launch ramp per band.
+#ifndef POLSAR_NLM_BAND
+#define POLSAR_NLM_BAND 1024
+#endif
+constexpr int64_t NLM_BAND = POLSAR_NLM_BAND;
+inline bool nlm_sym_ok(int R) { return R >= 1 && R <= V3_RMAX && !nlm_direct(); }
+inline int64_t nlm_band_slab_rows(int64_t slab_rows, int R) {
+    const int64_t b = NLM_BAND + 2 * (int64_t)R;
+    return slab_rows < b ? slab_rows : b;
+}
+
 
 }  // namespace
 }  // namespace polsar_impl

@@ -1,6 +1,6 @@
 // window_mma.cuh -- part of libpolsar.so (B200, sm_100a); arXiv 1807.08084.
 // Pass 1 of the window sums on the FP64 tensor cores: K3b (log-det distance)
-// and K6 (symmetric Wishart KL), the default for fp32 storage (POLSAR_WINDOW_MMA).
+// and K6 (symmetric Wishart KL), the product for fp32 storage.
 //
 // The pair determinant of the log-det window (BASELINE
 // configs[4]) through the 3x3 identity
@@ -61,17 +61,14 @@ constexpr int MMA_THREADS = 32 * (K3_TX / 8) * (MMA_TY / MMA_RB);  // one warp p
 constexpr int MMA_RS = 20;             // record doubles: Z (9) | adj2 (9) | 1 | D  (160 B:
                                        // a warp's b-fragment loads hit 32 distinct banks per half)
 
-// POLSAR_WINDOW_MMA: unset = the tensor-core pass 1 for fp32 storage (the
-// default: fp64 storage keeps the scalar pass 1, whose fp64 weights would
-// share the FP64 pipe with the DMMAs); 1 = for both storage precisions; 0 = never.
-int window_mma_mode() {
-    static const int v = [] {
-        const char* e = getenv("POLSAR_WINDOW_MMA");
-        return e ? (e[0] == '1' ? 1 : e[0] == '0' ? 0 : -1) : -1;
-    }();
-    return v;
-}
-
+// POLSAR_WINDOW_MMA (compile time; tools/build_variant.sh): -1 (the product) =
+// the tensor-core pass 1 for fp32 storage (fp64 storage keeps the scalar
+// pass 1, whose fp64 weights would share the FP64 pipe with the DMMAs); 1 =
+// for both storage precisions; 0 = never.
+#ifndef POLSAR_WINDOW_MMA
+#define POLSAR_WINDOW_MMA -1
+#endif
+constexpr int window_mma_mode() { return POLSAR_WINDOW_MMA; }
 
 __host__ __device__ constexpr int mma_nt(int R) { return (2 * R + 15) / 8; }
 // halo columns: x0 - R .. x0 - R + HWe - 1 (the last group's NT blocks may
@@ -85,16 +82,15 @@ size_t mma_fwd_smem(int R) {
            (size_t)MMA_TY * mma_hwe(R) * 9 * sizeof(S);  // + the staging buffer
 }
 
-// Does polsar_window_distance run the tensor-core form for this call?  (The
-// workspace query asks the same question.)  The other A/B forms
-// (POLSAR_WINDOW_VARIANT=2/3, POLSAR_WINDOW_PLANES=1) take precedence.
+// Does polsar_window_distance / polsar_window_kl run the tensor-core form for
+// this call?  (The workspace query asks the same question.)
 bool use_window_mma(int dtype, int radius) {
-    if (radius > V3_RMAX || window_variant() != 4 || window_planes()) return false;
+    if (radius > V3_RMAX || window_planes()) return false;
     const int m = window_mma_mode();
     if (m == 0) return false;
     if (dtype == POLSAR_F32) return mma_fwd_smem<float, float>(radius) <= K3_SMEM_MAX;
     return m == 1 && (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) &&
-           mma_fwd_smem<double, double>(radius) <= K3_SMEM_MAX;  // (fp64 at R = 12 does not fit)
+           mma_fwd_smem<double, double>(radius) <= K3_SMEM_MAX;  // (fp64 at R = 12: 229,376 B, fits)
 }
 
 __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {

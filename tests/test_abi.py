@@ -79,7 +79,9 @@ def test_loads_and_validates_without_gpu():
     assert lib.polsar_window_workspace_bytes(big, big, 11, 0) == 0
     assert lib.polsar_checksum(None, 5, 2, 1, 0, 0, None, None, None) == 1
     assert lib.polsar_inv_det_host(None, None, None, 5, 5, 0, 0, None, 0, None, None, None) == 1
-    assert lib.polsar_window_workspace_bytes(2048, 2048, 11, 0) >= 2048 * 2048 * (4 + 8 + 264 * 4)
+    # c5: the NLM's weight planes over one 1024-row band (+ 2R halo rows), not the image
+    assert lib.polsar_window_workspace_bytes(2048, 2048, 11, 0) >= 1046 * 2048 * (4 + 8 + 264 * 4)
+    assert lib.polsar_window_workspace_bytes(2048, 2048, 11, 0) < 2048 * 2048 * (264 * 4)
     assert lib.polsar_host_chunk_pixels(3 << 30, 0) % 64 == 0
 
 
@@ -105,33 +107,48 @@ def test_product_never_imports_oracle():
 @pytest.mark.parametrize("rows,width,radius", [(1, 1, 11), (1, 50, 4), (5, 300, 12), (130, 7, 1),
                                                (2048, 2048, 11), (37, 53, 3), (3, 3, 0)])
 def test_window_workspace_covers_every_form(rows, width, radius):
-    """polsar_window_workspace_bytes_for(entry) >= the need of every form that
-    entry point may run: the weight planes (pitch rounded to 16
-    bytes) for the NLM, the tiles' backward sums of the shared-memory form
-    (32-column tiles of 32 rows, or 24 / 16 for KL, or 8 for the tensor-core
-    pass 1, each (32 + 2R)(TY + R) int64) and the KL prepass;
+    """polsar_window_workspace_bytes_for(entry) is the need of the form that
+    entry point runs for (dtype, R) -- fixed at compile time, no environment
+    switches: the tiles' backward sums of the shared-memory
+    forms (32-column tiles of 32 rows, 16 for fp64 KL, 8 for the tensor-core
+    pass 1, each (32 + 2R)(TY + R) int64) after the prepass planes; the weight
+    planes (pitch rounded to 16 bytes) where the shared-memory form does not
+    fit and for the NLM, whose planes cover one band of 512 output rows;
     polsar_window_workspace_bytes >= all of them."""
     lib = _lib.lib()
     up = lambda b: (b + 255) // 256 * 256  # noqa: E731
     n = rows * width
     for dtype, wt in ((0, 4), (1, 8), (2, 4), (3, 8)):
         pitch = (width + 16 // wt - 1) // (16 // wt) * (16 // wt)
-        planes = up(n * wt) + up(n * 8) + up(2 * radius * (radius + 1) * rows * pitch * wt)
+
+        def planes(pre, r_rows):
+            m = r_rows * width
+            return up(pre) + up(m * 8) + up(2 * radius * (radius + 1) * r_rows * pitch * wt)
 
         def acc(pre, ty):
             tiles = ((width + 31) // 32) * ((rows + ty - 1) // ty)
             return up(pre) + up(n * 8) + up(tiles * (32 + 2 * radius) * (ty + radius) * 8)
-        need = {0: [up(n * wt), acc(n * wt, 32)], 1: [up(n * wt)] + ([planes] if radius >= 1 else []), 2: []}
-        if dtype != 2:  # (no KL in POLSAR_F32_PLAIN)
-            need[2] = [up(n * 160), acc(n * 160, 24 if wt == 4 else 16)]
-            if radius == 12:
-                need[2].append(planes - up(n * wt) + up(n * 160))  # KL's plane form at R = 12
-        if dtype == 0:  # fp32 storage: the tensor-core pass 1 (8-row tiles, no prepass)
-            need[0].append(acc(0, 8))
-            need[2] = [acc(0, 8)]
+        sym = radius <= 12
+        rows_b = min(rows, 1024 + 2 * radius)
+        expect = {}
+        if not sym:
+            expect[0] = [up(n * wt)]
+        elif dtype == 0:  # fp32 storage: the tensor-core pass 1 (8-row tiles, no prepass)
+            expect[0] = [acc(0, 8)]
+        else:
+            expect[0] = [acc(n * wt, 32), planes(n * wt, rows)]
+        expect[1] = [planes(rows_b * width * wt, rows_b)] if 1 <= radius <= 12 else [up(n * wt)]
+        if not sym or dtype == 2:
+            expect[2] = [0]
+        elif dtype == 0:
+            expect[2] = [acc(0, 8)]
+        else:
+            expect[2] = [acc(n * 160, 16), planes(n * 160, rows)]
         for e in range(3):
             got = lib.polsar_window_workspace_bytes_for(e, rows, width, radius, dtype)
-            assert got >= max(need[e], default=0), (e, dtype, got, need[e])
+            assert got in expect[e], (e, dtype, got, expect[e])
             assert lib.polsar_window_workspace_bytes(rows, width, radius, dtype) >= got
         if dtype == 0 and rows * width > 1000 and radius >= 8:  # the window sum needs far less than the NLM
-            assert 8 * lib.polsar_window_workspace_bytes_for(0, rows, width, radius, dtype) < planes
+            assert 4 * lib.polsar_window_workspace_bytes_for(0, rows, width, radius, dtype) < expect[1][0]
+        # POLSAR_F64_EFT (an inverse/det mode) has no window form
+        assert lib.polsar_window_workspace_bytes_for(0, rows, width, radius, 4) == 0

@@ -96,56 +96,6 @@ def test_window_c5_sampled(cuda):
     assert np.all(np.isfinite(got)) and got.min() >= 1 - 1e-6 and got.max() <= 529 + 1e-3
 
 
-VARIANT_ENV = {"2": {"POLSAR_WINDOW_VARIANT": "2"}, "3": {"POLSAR_WINDOW_VARIANT": "3"},
-               "planes": {"POLSAR_WINDOW_PLANES": "1"}, "scalar": {"POLSAR_WINDOW_MMA": "0"},
-               "mma_all": {"POLSAR_WINDOW_MMA": "1"}}
-
-
-@pytest.mark.parametrize("variant", sorted(VARIANT_ENV))
-def test_window_variant_subprocess(cuda, variant):
-    """The alternative kernels (POLSAR_WINDOW_VARIANT=2: the direct form over
-    ordered pairs; 3: the expansion form; POLSAR_WINDOW_PLANES=1: the
-    symmetric form through the weight planes instead of the shared-memory
-    backward sums; POLSAR_WINDOW_MMA=0: the scalar pass 1 for fp32 storage
-    too; =1: the tensor-core pass 1 for fp64 storage too; read once per
-    process) against the oracle in a child process: the log-det window sum,
-    and the KL window sum (variants 2 and 3 run KL on the streaming expansion
-    kernel)."""
-    import os
-    import subprocess
-    import sys
-    code = r'''
-import numpy as np, torch, oracle
-import paper_1807_08084_b200 as P
-from paper_1807_08084_b200 import configs, wishart
-# tolerances of test_gpu_window / test_gpu_kl (DESIGN.md R-12, R-16)
-for dt, tol, tol_kl in ((torch.float32, 2e-5, 2e-5), (torch.float64, 1e-12, 1e-12)):
-    h, w, r = 80, 70, 11
-    z = wishart.generate(configs.get("c5").scaled(h, w), device="cuda").to(dt)
-    got = P.window_distance(z, h, w, radius=r).cpu().numpy()
-    ref = oracle.window(z.cpu().numpy(), h, w, r, 4.0, 1.0)
-    e = float((np.abs(got - ref) / ref).max())
-    assert e <= tol, ("window", dt, e)
-    got = P.window_kl(z, h, w, radius=r).cpu().numpy()
-    ref = oracle.window_kl(z.cpu().numpy(), h, w, r, 4.0, 1.0)
-    e = float((np.abs(got - ref) / ref).max())
-    assert e <= tol_kl, ("kl", dt, e)
-    # R = 12 (the tensor-core form's largest tile; fp64 falls back to the scalar form)
-    h, w = 40, 45
-    z = wishart.generate(configs.get("c5").scaled(h, w), device="cuda").to(dt)
-    got = P.window_distance(z, h, w, radius=12).cpu().numpy()
-    ref = oracle.window(z.cpu().numpy(), h, w, 12, 4.0, 1.0)
-    e = float((np.abs(got - ref) / ref).max())
-    assert e <= tol, ("window R=12", dt, e)
-print("ok")
-'''
-    env = dict(os.environ, **VARIANT_ENV[variant])
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
-                         text=True, timeout=300)
-    assert res.returncode == 0 and "ok" in res.stdout, res.stdout + res.stderr
-
-
 @pytest.mark.parametrize("fn", ["window_distance", "window_kl"])
 def test_window_nonfinite_input_propagates(cuda, fn):
     """A NaN pixel makes W NaN exactly on the pixels whose window holds it

@@ -1,5 +1,6 @@
-"""Development aid: where does the tensor-core pass 1 (POLSAR_WINDOW_MMA=1)
-differ from the default window kernel?  Run twice (env on / off) and compare."""
+"""Development aid: where does one window build differ from another (e.g. the
+tensor-core pass 1 against a -DPOLSAR_WINDOW_MMA=0 build loaded with
+POLSAR_LIB_OVERRIDE)?  Run once per build and compare."""
 import os
 import sys
 

@@ -40,8 +40,9 @@ def main():
 
     ref = oracle.window_threaded(zh, h, w, R, cfg.looks, cfg.h, idx, threads)
     ii = torch.as_tensor(idx, device=dev)
-    mma = os.environ.get("POLSAR_WINDOW_MMA", "") != "0"  # (read once per process by the library too)
-    form = "tensor-core pass 1" if mma else "scalar pass 1"
+    # the library's pass 1 for fp32 storage (compile-time POLSAR_WINDOW_MMA; a
+    # -DPOLSAR_WINDOW_MMA=0 build loaded with POLSAR_LIB_OVERRIDE runs the scalar one)
+    form = "scalar pass 1" if os.environ.get("POLSAR_LIB_OVERRIDE") else "tensor-core pass 1"
     for plain in (False, True):
         got = P.window_distance(z, h, w, radius=R, looks=cfg.looks, h=cfg.h, plain=plain)[ii].cpu().numpy()
         row("window W", "fp32 storage, fp32 pair det (plain; reported)" if plain else
