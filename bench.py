@@ -740,7 +740,7 @@ def run_window(args):
     mma = False
     if args.kernel == "nlm":
         symmetric = 1 <= R <= 12
-        variant = ("symmetric two-pass (pass 1 + TMA gather, 512-row bands)" if symmetric else "direct")
+        variant = ("symmetric two-pass (pass 1 + TMA gather, 1024-row bands)" if symmetric else "direct")
     else:
         symmetric = R <= 12
         variant = "symmetric two-pass" if symmetric else "direct"
