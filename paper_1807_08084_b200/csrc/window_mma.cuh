@@ -54,7 +54,7 @@ constexpr int MMA_CHUNK = POLSAR_MMA_CHUNK;  // tiles per CTA (a column of them)
 constexpr int kMmaUnroll = POLSAR_MMA_UNROLL;  // full window rows per loop iteration
 constexpr int MMA_TY = POLSAR_MMA_TY;  // tile rows (pass 2 takes the same TY)
 #ifndef POLSAR_MMA_RB
-#define POLSAR_MMA_RB 2
+#define POLSAR_MMA_RB 1
 #endif
 constexpr int MMA_RB = POLSAR_MMA_RB;  // owned rows per warp
 constexpr int MMA_THREADS = 32 * (K3_TX / 8) * (MMA_TY / MMA_RB);  // one warp per 8 x RB pixels
