@@ -350,7 +350,7 @@ def run_ours(args):
     checksum = int(res[0].item()) & 0xFFFFFFFFFFFFFFFF
     counts = [int(x) for x in res[1:].tolist()]
 
-    total = n * world
+    total = H * cfg.width  # every pixel of the image, over all ranks (shards may differ by a row)
     value = total * args.steps / t_max
     ms_per_step = t_max / args.steps * 1e3
     line = {
