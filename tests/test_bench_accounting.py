@@ -64,3 +64,39 @@ def test_default_is_the_whole_baseline_image(bench, monkeypatch):
         rows.extend(range(r0, r1))
     assert rows == list(range(cfg.height))
     assert "whole image sharded" in bench.workload_name(cfg, args, 8)
+
+
+def _run(cmd, env=None):
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable] + cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env=env)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    return [json.loads(l) for l in lines]
+
+
+def test_reference_arm_line():
+    """`bench.py --impl reference` (CPU only: the oracle's storage-precision
+    build on the host cores) prints one JSON line with the contract's keys."""
+    (line,) = _run(["bench.py", "--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "1"])
+    assert line["impl"] == "reference" and line["unit"] == "matrices/s" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["gpu_launches"] == 0
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["config"]["workload"].startswith("c1: BASELINE configs[0]")
+    assert line["paper_table2_context"]["simulated_5469354"]["proposed_ms"]["t_avg"] == 231.51
+
+
+def test_reference_arm_under_torchrun():
+    """Under torchrun only rank 0 runs and prints; the other ranks exit 0."""
+    import os
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    lines = _run(["-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+                  "127.0.0.1", "--master-port", str(port), "bench.py", "--impl", "reference", "--gpus", "2",
+                  "--config", "c1", "--steps", "1", "--warmup", "1"], env=dict(os.environ, OMP_NUM_THREADS="1"))
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2
