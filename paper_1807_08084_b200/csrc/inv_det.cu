@@ -38,10 +38,6 @@ struct Vec2f {
     typedef float2 type;
     static constexpr int n = 2;
 };
-struct Vec1f {
-    typedef float type;
-    static constexpr int n = 1;
-};
 template <typename S, int ALGO>
 struct VecSel {
     typedef Vec<S> V;
@@ -58,8 +54,6 @@ __device__ __forceinline__ void unpack<float2, float>(const float2& v, float* x)
     x[0] = v.x; x[1] = v.y;
 }
 template <>
-__device__ __forceinline__ void unpack<float, float>(const float& v, float* x) { x[0] = v; }
-template <>
 __device__ __forceinline__ void unpack<float4, float>(const float4& v, float* x) {
     x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
 }
@@ -72,7 +66,6 @@ __device__ __forceinline__ double2 pack2(const double* x) { return make_double2(
 __device__ __forceinline__ float4 packv(const float* x, float4*) { return pack4(x); }
 __device__ __forceinline__ double2 packv(const double* x, double2*) { return pack2(x); }
 __device__ __forceinline__ float2 packv(const float* x, float2*) { return make_float2(x[0], x[1]); }
-__device__ __forceinline__ float packv(const float* x, float*) { return x[0]; }
 
 constexpr int K1_THREADS = 128;
 
