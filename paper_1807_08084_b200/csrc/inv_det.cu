@@ -69,12 +69,21 @@ __device__ __forceinline__ float2 packv(const float* x, float2*) { return make_f
 
 constexpr int K1_THREADS = 128;
 
+// (POLSAR_K2_MINB: an A/B register cap for Alg. 1 through __launch_bounds__'
+// min-blocks argument; 0 = none -- an explicit 1 alone changes ptxas's register
+// budget: 82 instead of 76 registers, 5 instead of 6 CTAs per SM, K2 6 % slower)
 #ifndef POLSAR_K2_MINB
-#define POLSAR_K2_MINB 1
+#define POLSAR_K2_MINB 0
+#endif
+#if POLSAR_K2_MINB > 0
+#define K1_LAUNCH_BOUNDS(ALGO) __launch_bounds__(K1_THREADS, (ALGO) == 1 ? POLSAR_K2_MINB : 1)
+#else
+#define K1_LAUNCH_BOUNDS(ALGO) __launch_bounds__(K1_THREADS)
 #endif
 #ifndef K2_U
 #define K2_U 1
 #endif
+
 // Vector groups per thread (compile-time A/B knob K2_U; 1 = the product):
 // U > 1 gives each thread U independent groups (ILP for Alg. 1's serial
 // DSQRT / DRCP chains) while every load and store instruction of a warp still
@@ -87,16 +96,65 @@ struct GroupsPerThread {
 };
 
 template <typename S, int ALGO, int MATH>
-__global__ void __launch_bounds__(K1_THREADS, ALGO == 1 ? POLSAR_K2_MINB : 1)
+__device__ __forceinline__ void store_status(uint8_t* status, int64_t p, const uint8_t* st) {
+    constexpr int W = VecSel<S, ALGO>::V::n;
+    if constexpr (W == 4) {
+        uint32_t w = (uint32_t)st[0] | ((uint32_t)st[1] << 8) | ((uint32_t)st[2] << 16) | ((uint32_t)st[3] << 24);
+        *reinterpret_cast<uint32_t*>(status + p) = w;
+    } else if constexpr (W == 2) {
+        *reinterpret_cast<uint16_t*>(status + p) = (uint16_t)(st[0] | (st[1] << 8));
+    } else {
+        status[p] = st[0];
+    }
+}
+
+// The product body: each thread one vector group (VEC pixels), one 16-byte
+// vector per input plane (9 x LDG.128) and per output plane (11 x STG.128) +
+// VEC status bytes, over a whole-batch grid (grid-stride for the remainder).
+template <typename S, int ALGO, int MATH>
+__global__ void K1_LAUNCH_BOUNDS(ALGO)
 k_inv_det_vec(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
+              int64_t n_groups, int64_t ld) {
+    typedef typename VecSel<S, ALGO>::V VV;
+    typedef typename VV::type V;
+    constexpr int W = VV::n;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_groups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = g * W;
+        POLSAR_CHECK(p + W <= n_groups * W && p % W == 0);
+        S in[9][W];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) unpack<V, S>(ld_stream(reinterpret_cast<const V*>(z + k * ld + p)), in[k]);
+        S res[11][W];
+        uint8_t st[W];
+#pragma unroll
+        for (int v = 0; v < W; ++v) {
+            S x[9], y[11];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) x[k] = in[k][v];
+            solve_one<S, ALGO, MATH>(x, y, st[v]);
+#pragma unroll
+            for (int k = 0; k < 11; ++k) res[k][v] = y[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 11; ++k)
+            st_stream(reinterpret_cast<V*>(out + k * ld + p), packv(res[k], (V*)nullptr));
+        if (status) store_status<S, ALGO, MATH>(status, p, st);
+    }
+}
+
+// A/B body (K2_U > 1 for Alg. 1, see above): U groups per thread in warp chunks.
+template <typename S, int ALGO, int MATH>
+__global__ void K1_LAUNCH_BOUNDS(ALGO)
+k_inv_det_vec_u(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
               int64_t n_groups, int64_t ld) {
     typedef typename VecSel<S, ALGO>::V VV;
     typedef typename VV::type V;
     constexpr int W = VV::n;
     constexpr int U = GroupsPerThread<ALGO>::U;
     const int64_t n_slots = (n_groups + U - 1) / U;  // thread slots: one per U groups
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ((n_slots + 31) & ~(int64_t)31);
-         t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t_end = (n_slots + 31) & ~(int64_t)31;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < t_end; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t g0 = (t & ~(int64_t)31) * U + (t & 31);  // this lane's first group
         S in[U][9][W];
 #pragma unroll
@@ -182,8 +240,14 @@ int launch_inv_det(const void* zv, void* outv, uint8_t* status, int64_t n, int64
     if (n_vec > 0) {
         int64_t groups = n_vec / W;
         constexpr int U = GroupsPerThread<ALGO>::U;
-        const int64_t slots = ((groups + U - 1) / U + 31) & ~(int64_t)31;
-        k_inv_det_vec<S, ALGO, MATH><<<grid_full(slots, K1_THREADS), K1_THREADS, 0, s>>>(z, out, status, groups, ld);
+        if constexpr (U == 1) {
+            k_inv_det_vec<S, ALGO, MATH><<<grid_full(groups, K1_THREADS), K1_THREADS, 0, s>>>(z, out, status, groups,
+                                                                                               ld);
+        } else {
+            const int64_t slots = ((groups + U - 1) / U + 31) & ~(int64_t)31;
+            k_inv_det_vec_u<S, ALGO, MATH><<<grid_full(slots, K1_THREADS), K1_THREADS, 0, s>>>(z, out, status,
+                                                                                               groups, ld);
+        }
     }
     if (n > n_vec) {
         k_inv_det_scalar<S, ALGO, MATH>
