@@ -241,8 +241,12 @@ int launch_inv_det(const void* zv, void* outv, uint8_t* status, int64_t n, int64
         int64_t groups = n_vec / W;
         constexpr int U = GroupsPerThread<ALGO>::U;
         if constexpr (U == 1) {
-            k_inv_det_vec<S, ALGO, MATH><<<grid_full(groups, K1_THREADS), K1_THREADS, 0, s>>>(z, out, status, groups,
-                                                                                               ld);
+#ifdef POLSAR_K2_GRID_CAP  // A/B: a capped (grid-stride) grid for Alg. 1
+            const int grid = ALGO == 1 ? grid_for(groups, K1_THREADS) : grid_full(groups, K1_THREADS);
+#else
+            const int grid = grid_full(groups, K1_THREADS);
+#endif
+            k_inv_det_vec<S, ALGO, MATH><<<grid, K1_THREADS, 0, s>>>(z, out, status, groups, ld);
         } else {
             const int64_t slots = ((groups + U - 1) / U + 31) & ~(int64_t)31;
             k_inv_det_vec_u<S, ALGO, MATH><<<grid_full(slots, K1_THREADS), K1_THREADS, 0, s>>>(z, out, status,
