@@ -422,7 +422,7 @@ def measure_e2e(args, P, torch, dist, world, z, n_full, tdt, esz, dev, cfg):
     zh.copy_(z[:, :n])
     oh = torch.empty((11, n), dtype=tdt).pin_memory()
     sh = torch.empty(n, dtype=torch.uint8).pin_memory()
-    ws = torch.empty(3 << 30, dtype=torch.uint8, device=dev)
+    ws = torch.empty(3 << 28, dtype=torch.uint8, device=dev)  # 0.75 GB: 3M-px chunks (tools/e2e_sweep.py)
     streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
     algo = 0 if args.algo == "adjugate" else 1
     P.polsar_inv_det_host(zh, oh, sh, ws, streams, algo=algo, plain=args.plain)  # warm-up
