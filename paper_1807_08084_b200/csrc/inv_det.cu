@@ -80,21 +80,6 @@ constexpr int K1_THREADS = 128;
 #else
 #define K1_LAUNCH_BOUNDS(ALGO) __launch_bounds__(K1_THREADS)
 #endif
-#ifndef K2_U
-#define K2_U 1
-#endif
-
-// Vector groups per thread (compile-time A/B knob K2_U; 1 = the product):
-// U > 1 gives each thread U independent groups (ILP for Alg. 1's serial
-// DSQRT / DRCP chains) while every load and store instruction of a warp still
-// covers 32 consecutive groups: warp chunk c holds groups [32 U c, 32 U (c+1))
-// and lane l takes 32 U c + 32 j + l, j < U.  Measured on B200:
-// U = 2 or 4 and 4-pixel groups for Alg. 1 are slower than U = 1.
-template <int ALGO>
-struct GroupsPerThread {
-    static constexpr int U = ALGO == 1 ? K2_U : 1;
-};
-
 template <typename S, int ALGO, int MATH>
 __device__ __forceinline__ void store_status(uint8_t* status, int64_t p, const uint8_t* st) {
     constexpr int W = VecSel<S, ALGO>::V::n;
@@ -143,72 +128,6 @@ k_inv_det_vec(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict_
     }
 }
 
-// A/B body (K2_U > 1 for Alg. 1, see above): U groups per thread in warp chunks.
-template <typename S, int ALGO, int MATH>
-__global__ void K1_LAUNCH_BOUNDS(ALGO)
-k_inv_det_vec_u(const S* __restrict__ z, S* __restrict__ out, uint8_t* __restrict__ status,
-              int64_t n_groups, int64_t ld) {
-    typedef typename VecSel<S, ALGO>::V VV;
-    typedef typename VV::type V;
-    constexpr int W = VV::n;
-    constexpr int U = GroupsPerThread<ALGO>::U;
-    const int64_t n_slots = (n_groups + U - 1) / U;  // thread slots: one per U groups
-    const int64_t t_end = (n_slots + 31) & ~(int64_t)31;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < t_end; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t g0 = (t & ~(int64_t)31) * U + (t & 31);  // this lane's first group
-        S in[U][9][W];
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const int64_t p = (g0 + 32 * j) * W;
-            if (g0 + 32 * j < n_groups) {
-#pragma unroll
-                for (int k = 0; k < 9; ++k)
-                    unpack<V, S>(ld_stream(reinterpret_cast<const V*>(z + k * ld + p)), in[j][k]);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 9; ++k)
-#pragma unroll
-                    for (int v = 0; v < W; ++v) in[j][k][v] = S(k == 0 || k == 5 || k == 8);
-            }
-        }
-        S res[U][11][W];
-        uint8_t st[U][W];
-#pragma unroll
-        for (int j = 0; j < U; ++j)
-#pragma unroll
-            for (int v = 0; v < W; ++v) {
-                S x[9], y[11];
-#pragma unroll
-                for (int k = 0; k < 9; ++k) x[k] = in[j][k][v];
-                solve_one<S, ALGO, MATH>(x, y, st[j][v]);
-#pragma unroll
-                for (int k = 0; k < 11; ++k) res[j][k][v] = y[k];
-            }
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const int64_t g = g0 + 32 * j;
-            if (g >= n_groups) continue;
-            const int64_t p = g * W;
-            POLSAR_CHECK(p + W <= n_groups * W && p % W == 0);
-#pragma unroll
-            for (int k = 0; k < 11; ++k)
-                st_stream(reinterpret_cast<V*>(out + k * ld + p), packv(res[j][k], (V*)nullptr));
-            if (status) {
-                if constexpr (W == 4) {
-                    uint32_t w = (uint32_t)st[j][0] | ((uint32_t)st[j][1] << 8) | ((uint32_t)st[j][2] << 16) |
-                                 ((uint32_t)st[j][3] << 24);
-                    *reinterpret_cast<uint32_t*>(status + p) = w;
-                } else if constexpr (W == 2) {
-                    uint16_t w = (uint16_t)(st[j][0] | (st[j][1] << 8));
-                    *reinterpret_cast<uint16_t*>(status + p) = w;
-                } else {
-                    status[p] = st[j][0];
-                }
-            }
-        }
-    }
-}
-
 // Scalar path: misaligned planes and the ragged tail; same solve_one.
 template <typename S, int ALGO, int MATH>
 __global__ void __launch_bounds__(256)
@@ -239,19 +158,7 @@ int launch_inv_det(const void* zv, void* outv, uint8_t* status, int64_t n, int64
     int64_t n_vec = aligned ? (n / W) * W : 0;
     if (n_vec > 0) {
         int64_t groups = n_vec / W;
-        constexpr int U = GroupsPerThread<ALGO>::U;
-        if constexpr (U == 1) {
-#ifdef POLSAR_K2_GRID_CAP  // A/B: a capped (grid-stride) grid for Alg. 1
-            const int grid = ALGO == 1 ? grid_for(groups, K1_THREADS) : grid_full(groups, K1_THREADS);
-#else
-            const int grid = grid_full(groups, K1_THREADS);
-#endif
-            k_inv_det_vec<S, ALGO, MATH><<<grid, K1_THREADS, 0, s>>>(z, out, status, groups, ld);
-        } else {
-            const int64_t slots = ((groups + U - 1) / U + 31) & ~(int64_t)31;
-            k_inv_det_vec_u<S, ALGO, MATH><<<grid_full(slots, K1_THREADS), K1_THREADS, 0, s>>>(z, out, status,
-                                                                                               groups, ld);
-        }
+        k_inv_det_vec<S, ALGO, MATH><<<grid_full(groups, K1_THREADS), K1_THREADS, 0, s>>>(z, out, status, groups, ld);
     }
     if (n > n_vec) {
         k_inv_det_scalar<S, ALGO, MATH>
