@@ -152,3 +152,15 @@ def test_window_workspace_covers_every_form(rows, width, radius):
             assert 4 * lib.polsar_window_workspace_bytes_for(0, rows, width, radius, dtype) < expect[1][0]
         # POLSAR_F64_EFT (an inverse/det mode) has no window form
         assert lib.polsar_window_workspace_bytes_for(0, rows, width, radius, 4) == 0
+
+
+def test_product_reads_no_environment():
+    """every kernel form of libpolsar.so is fixed at compile
+    time (A/B alternatives are -D builds); the library neither calls getenv nor
+    mentions it in its sources."""
+    csrc = os.path.join(ROOT, "paper_1807_08084_b200", "csrc")
+    for f in os.listdir(csrc):
+        assert "getenv" not in open(os.path.join(csrc, f)).read(), f
+    so = _build.build_target("libpolsar")
+    syms = subprocess.run(["nm", "-D", "--undefined-only", so], capture_output=True, text=True).stdout
+    assert "getenv" not in syms
