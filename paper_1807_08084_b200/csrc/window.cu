@@ -27,7 +27,7 @@ size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t w
     // dispatch below, fixed at compile time (no environment switches)
     if (entry == 0) {  // polsar_window_distance
         if (!sym_ok) return up((size_t)n * wt);  // the direct form: one plane of g
-        if (use_window_mma(dtype, radius)) return mma_sym_bytes(slab_rows, width, radius);
+        if (use_window_mma(dtype, radius, false)) return mma_sym_bytes(slab_rows, width, radius);
         return window_sym_need(dtype, slab_rows, width, radius);
     }
     if (entry == 1) {  // polsar_nlm_filter
@@ -37,7 +37,7 @@ size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t w
     }
     // polsar_window_kl (radius <= 12; no fp32-arithmetic mode)
     if (dtype == POLSAR_F32_PLAIN || !sym_ok) return 0;
-    if (use_window_mma(dtype, radius)) return mma_sym_bytes(slab_rows, width, radius);
+    if (use_window_mma(dtype, radius, true)) return mma_sym_bytes(slab_rows, width, radius);
     return kl_sym_need(dtype, slab_rows, width, radius);
 }
 
@@ -60,7 +60,7 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
     if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
     if (!z || !workspace || !out) return fail(POLSAR_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    if (use_window_mma(dtype, radius))
+    if (use_window_mma(dtype, radius, false))
         return dtype == POLSAR_F32
                    ? launch_window_mma<float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end, radius,
                                                      looks, h, workspace, out, s)
@@ -102,7 +102,7 @@ int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows
     if (width == 0 || out_row_end == out_row_begin) return POLSAR_OK;
     if (!z || !workspace || !out) return fail(POLSAR_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    if (use_window_mma(dtype, radius))
+    if (use_window_mma(dtype, radius, true))
         return dtype == POLSAR_F32
                    ? launch_window_kl_mma<float, float>(z, ld, width, slab_rows, out_row_begin, out_row_end, radius,
                                                         looks, h, workspace, out, s)

@@ -62,9 +62,8 @@ constexpr int MMA_RS = 20;             // record doubles: Z (9) | adj2 (9) | 1 |
                                        // a warp's b-fragment loads hit 32 distinct banks per half)
 
 // POLSAR_WINDOW_MMA (compile time; tools/build_variant.sh): -1 (the product) =
-// the tensor-core pass 1 for fp32 storage (fp64 storage keeps the scalar
-// pass 1, whose fp64 weights would share the FP64 pipe with the DMMAs); 1 =
-// for both storage precisions; 0 = never.
+// the tensor-core pass 1 for fp32 storage, and for the fp64 KL window (see
+// use_window_mma); 1 = for every call; 0 = never.
 #ifndef POLSAR_WINDOW_MMA
 #define POLSAR_WINDOW_MMA -1
 #endif
@@ -82,14 +81,18 @@ size_t mma_fwd_smem(int R) {
            (size_t)MMA_TY * mma_hwe(R) * 9 * sizeof(S);  // + the staging buffer
 }
 
-// Does polsar_window_distance / polsar_window_kl run the tensor-core form for
-// this call?  (The workspace query asks the same question.)
-bool use_window_mma(int dtype, int radius) {
+// Does polsar_window_distance (kl = false) / polsar_window_kl (kl = true) run
+// the tensor-core form for this call?  (The workspace query asks the same
+// question.)  fp32 storage: both.  fp64 storage: the KL window (4.78 vs 5.33 ms
+// on c5: its per-pair weight is one exp, so the DMMAs keep the FP64 datapath),
+// not the log-det window (3.84 vs 3.49 ms: its fp64 weight's DFMA Newton
+// steps share the datapath with the DMMAs); POLSAR_WINDOW_MMA=1 forces both.
+bool use_window_mma(int dtype, int radius, bool kl) {
     if (radius > V3_RMAX || window_planes()) return false;
     const int m = window_mma_mode();
     if (m == 0) return false;
     if (dtype == POLSAR_F32) return mma_fwd_smem<float, float>(radius) <= K3_SMEM_MAX;
-    return m == 1 && (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) &&
+    return (m == 1 || kl) && (dtype == POLSAR_F64 || dtype == POLSAR_F64_PLAIN) &&
            mma_fwd_smem<double, double>(radius) <= K3_SMEM_MAX;  // (fp64 at R = 12: 229,376 B, fits)
 }
 
