@@ -135,4 +135,5 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0,
         "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+
 }  // namespace polsar_impl
