@@ -135,3 +135,27 @@ def test_workspace_for_entry_is_enough(cuda, entry, radius, shape, dt):
     torch.cuda.synchronize()
     assert bool((buf[need:] == 0xAB).all())
     assert bool(torch.isfinite(out).all()) and float(out.min()) >= 1 - 1e-6
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("shape,radius", [((50, 1), 11), ((1, 1), 11), ((2, 3), 11), ((13, 2), 5), ((1, 33), 12)])
+def test_window_degenerate_shapes(cuda, dt, shape, radius):
+    """Single-column, single-pixel and sub-tile images (the window clipped
+    to the image on every side): W, KL and NLM against the oracle."""
+    h, w = shape
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda).to(dt)
+    zh = z.cpu().numpy()
+    idx = np.arange(h * w)
+    tol = TOL[dt]
+    got = P.window_distance(z, h, w, radius=radius).cpu().numpy()
+    ref = oracle.window(zh, h, w, radius, 4.0, 1.0, idx)
+    assert (np.abs(got - ref) / ref).max() <= tol
+    got = P.window_kl(z, h, w, radius=radius).cpu().numpy()
+    ref = oracle.window_kl(zh, h, w, radius, 4.0, 1.0, idx)
+    assert (np.abs(got - ref) / ref).max() <= tol
+    zhat, W = P.nlm_filter(z, h, w, radius=radius)
+    rz, rw = oracle.nlm(zh, h, w, radius, 4.0, 1.0, idx)
+    err = np.max(np.abs(zhat.cpu().numpy().astype(np.float64) - rz), axis=0) / np.max(np.abs(rz), axis=0)
+    assert err.max() <= tol and (np.abs(W.cpu().numpy() - rw) / rw).max() <= tol
+    if h * w == 1:
+        assert float(W[0]) == 1.0 and torch.equal(zhat[:, 0], z[:, 0])
