@@ -62,6 +62,9 @@ def parse():
                    help="window kernels at N > 1: regenerate halo rows locally or exchange them (NCCL)")
     p.add_argument("--rows", type=int, default=0,
                    help="override rows per GPU (profiling runs only; not a bench line)")
+    p.add_argument("--functional-1gpu", action="store_true",
+                   help="test only: run every torchrun rank on cuda:0 with gloo (checks the N > 1 host "
+                        "logic on a one-GPU box; not a measurement)")
     return p.parse_args()
 
 
@@ -146,6 +149,24 @@ def setup_dist(args):
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     return world, rank, local
+
+
+def init_ranks(world, local):
+    """One process per GPU over NCCL.  (--functional-1gpu: every rank on
+    cuda:0 with gloo collectives -- a host-logic check of the N > 1 path on a
+    one-GPU box, never a measurement: the ranks share one GPU.)"""
+    import torch
+    import torch.distributed as dist
+    if ARGS.functional_1gpu:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        if ARGS.functional_1gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    return dev
 
 
 def rows_for(rank, world, cfg, scaling):
@@ -274,10 +295,7 @@ def run_ours(args):
     from paper_1807_08084_b200 import configs, wishart
 
     world, rank, local = setup_dist(args)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_ranks(world, local)
 
     cfg = configs.get(args.config)
     if cfg.radius:
@@ -674,10 +692,7 @@ def run_window(args):
     from paper_1807_08084_b200 import dist as pdist
 
     world, rank, local = setup_dist(args)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_ranks(world, local)
     cfg = configs.get("c5")
     if args.rows:
         cfg = cfg.scaled(args.rows)
@@ -822,8 +837,13 @@ def unordered_pairs_rows(h, w, r, r0, r1):
     return a - b // 2
 
 
+ARGS = None
+
+
 def main():
+    global ARGS
     args = parse()
+    ARGS = args
     if args.impl == "reference":
         return run_reference(args)
     if args.kernel != "inv_det":
