@@ -43,11 +43,14 @@ def main():
         zh = z.cpu().numpy()
         ref = oracle.inv_det_threaded(zh, threads)
         k = oracle.kappa2(zh)
-        for kname, algo, plain in (("Alg. 2 (default)", "adjugate", False),
-                                   ("Alg. 2 as printed", "adjugate", True),
-                                   ("Alg. 1 (default)", "cholesky", False),
-                                   ("Alg. 1 as printed (l21 fixed)", "cholesky", True)):
-            out, _ = P.inv_det(z, algo=algo, plain=plain)
+        modes = [("Alg. 2 (default)", "adjugate", False, False),
+                 ("Alg. 2 as printed", "adjugate", True, False),
+                 ("Alg. 1 (default)", "cholesky", False, False),
+                 ("Alg. 1 as printed (l21 fixed)", "cholesky", True, False)]
+        if z.dtype == torch.float64:
+            modes.insert(1, ("Alg. 2 error-free (POLSAR_F64_EFT)", "adjugate", False, True))
+        for kname, algo, plain, eft in modes:
+            out, _ = P.inv_det(z, algo=algo, plain=plain, eft=eft)
             got = out.cpu().numpy().astype(np.float64)
             inv = np.max(np.abs(got[:9] - ref[:9]), axis=0) / np.max(np.abs(ref[:9]), axis=0)
             det = np.abs(got[9] - ref[9]) / np.abs(ref[9])

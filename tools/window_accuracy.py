@@ -50,7 +50,7 @@ def main():
     z64 = z.double()
     got = P.window_distance(z64, h, w, radius=R, looks=cfg.looks, h=cfg.h)[ii].cpu().numpy()
     ref64 = oracle.window_threaded(z64.cpu().numpy(), h, w, R, cfg.looks, cfg.h, idx, threads)
-    row("window W", "fp64 storage", "4e-10", np.abs(got - ref64) / ref64)
+    row("window W", "fp64 storage", "1e-12", np.abs(got - ref64) / ref64)
     refk = oracle.window_kl_threaded(zh, h, w, R, cfg.looks, cfg.h, idx, threads)
     got = P.window_kl(z, h, w, radius=R, looks=cfg.looks, h=cfg.h)[ii].cpu().numpy()
     row("KL window W", f"fp32 storage, fp64 trace products ({form})", "2e-5", np.abs(got - refk) / refk)
