@@ -146,3 +146,18 @@ def test_nlm_nonfinite_input_propagates(cuda):
     near = (np.abs(ys - yb) <= r) & (np.abs(xs - xb) <= r)
     assert np.all(np.isnan(W[near])) and np.all(np.isfinite(W[~near]))
     assert np.all(np.isnan(zh[:, near])) and np.all(np.isfinite(zh[:, ~near]))
+
+
+@pytest.mark.parametrize("radius", [11, 0])
+def test_nlm_without_w_output(cuda, radius):
+    """out_w = NULL (W not wanted): Zhat is the same bits as with W, for the
+    symmetric (banded gather) form and the direct form (R = 0)."""
+    h, w = 40, 70
+    z = wishart.generate(configs.get("c5").scaled(h, w), device=cuda)
+    zhat, _ = P.nlm_filter(z, h, w, radius=radius)
+    ws = torch.empty(P.polsar_window_workspace_bytes_for(P.NLM, h, w, radius, P.POLSAR_F32), dtype=torch.uint8,
+                     device=cuda)
+    out = torch.empty_like(zhat)
+    P.polsar_nlm_filter(z, w, h, 0, h, radius, 4.0, 1.0, ws, out, None)
+    torch.cuda.synchronize()
+    assert torch.equal(out, zhat)
