@@ -116,18 +116,20 @@ int polsar_inv_det_blocks(const void* z, void* out, uint8_t* status, int64_t n, 
  * entry points (polsar_window_distance, polsar_nlm_filter, polsar_window_kl)
  * need for a slab of slab_rows x width pixels at this radius and dtype: the
  * largest need of the three.  (polsar_nlm_filter stores the 2R(R+1) forward
- * pair weights of every pixel, ~1.07 KB per pixel at R = 11 with fp32
- * weights; the default window and KL kernels need ~40 B per pixel.) */
+ * pair weights of the pixels of one band of 1024 output rows plus its 2R
+ * halo rows, ~1.07 KB per band pixel at R = 11 with fp32 weights -- 2.3 GB
+ * for a 2048-pixel-wide slab of any height; the window and KL kernels need
+ * ~40 B per slab pixel.) */
 size_t polsar_window_workspace_bytes(int64_t slab_rows, int64_t width, int radius, int dtype);
 
 /* polsar_window_workspace_bytes_for -- the same for one entry point:
  * entry 0 polsar_window_distance, 1 polsar_nlm_filter, 2 polsar_window_kl
  * (0 for an invalid entry, negative or > 2^40-pixel sizes, or an
- * unsupported dtype / radius).  A workspace of
- * this size serves every call of that entry point with these sizes in this
- * process.  The window and KL sums need ~40 B per pixel, so a UAVSAR-scale
- * slab (4e8 pixels) fits where the NLM's weight planes (~1 KB per pixel)
- * cannot. */
+ * unsupported dtype / radius).  It is the need of the kernel form that entry
+ * point runs for (dtype, radius) -- fixed at compile time, independent of the
+ * environment -- so a workspace of this size serves every call of that entry
+ * point with these sizes.  A UAVSAR-scale slab (10000 x 40000 pixels) needs
+ * ~16 GB for the window and KL sums and ~46 GB for the NLM (one band). */
 size_t polsar_window_workspace_bytes_for(int entry, int64_t slab_rows, int64_t width, int radius,
                                          int dtype);
 
@@ -162,8 +164,9 @@ int polsar_window_distance(const void* z, int64_t ld, int64_t width, int64_t sla
  * Kullback-Leibler distance (one of the divergences that need Z^-1, PAPER.md:
  * 70-76 [§I]):
  *   d_ij = L [ (tr(Z_i^-1 Z_j) + tr(Z_j^-1 Z_i)) / 2 - 3 ],  W_i = sum_j exp(-d_ij / h).
- * Z^-1 of every slab pixel comes from Alg. 2 (K1's device function) in a
- * prepass; each pair is then two 9-term trace products in fp64.  Arguments,
+ * Z^-1 of every slab pixel comes from Alg. 2 (K1's device function); each
+ * pair is then two 9-term trace products in fp64 (as one 20-term product on
+ * the FP64 tensor cores).  Arguments,
  * workspace (polsar_window_workspace_bytes_for(2, ...)) and errors as
  * polsar_window_distance; radius <= 12; dtype POLSAR_F32 or POLSAR_F64
  * (POLSAR_F32_PLAIN returns ENOTSUP). */
@@ -173,7 +176,10 @@ int polsar_window_kl(const void* z, int64_t ld, int64_t width, int64_t slab_rows
 
 /* polsar_nlm_filter -- non-local-means filter output with the same search-
  * window weights (the NLM filter with stochastic distances of PAPER.md:77-80
- * [§I]), fused into the window pass:
+ * [§I]); for 1 <= R <= 12 the symmetric pass stores each
+ * forward weight once and a gather pass forms Zhat, band by band (1024 output
+ * rows per band, each with its own R-row halos; the bands give the same bits
+ * as one pass over the slab would):
  *   W_i = sum_j exp(-d_ij / h),   Zhat_i = sum_j exp(-d_ij / h) Z_j / W_i.
  * Arguments as polsar_window_distance, plus
  *   out_w  : device, (e - b) x width values of W, or NULL
